@@ -1,0 +1,765 @@
+// capi.cu -- the extern "C" boundary (include/lamg_b200.h).
+//
+// Every entry point catches the library's C++ exceptions and returns the
+// status code of the reference exception type, with the reference's message
+// available from lamg_last_error().
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "solve.cuh"
+
+using namespace lamgb;
+
+namespace lamgb {
+uint64_t rng_derive_host(uint64_t seed, uint64_t stream);
+}
+
+struct lamg_ctx {
+  Ctx c;
+};
+struct lamg_hier {
+  std::unique_ptr<DHier> h;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return LAMG_OK;
+  } catch (const LamgError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return LAMG_E_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LAMG_E_ERROR;
+  }
+}
+
+void set_device(Ctx& c) { CK(cudaSetDevice(c.device)); }
+
+// host CSR -> owning device CSR
+void upload_csr(Ctx& c, const lamg_csr* a, DCSR& d) {
+  if (!a) throw LamgError(LAMG_E_ARGUMENT, "null CSR");
+  d.alloc(a->n, a->m, c.s);
+  d.rp.upload(a->row_ptr, a->n + 1);
+  d.col.upload(a->col, 2 * a->m);
+  d.val.upload(a->val, 2 * a->m);
+  d.diag.upload(a->diag, a->n);
+}
+
+void download_csr(Ctx& c, const DCSR& d, int64_t* rp, int32_t* col, double* val, double* diag) {
+  if (rp) d.rp.download(rp, d.n + 1);
+  if (col) d.col.download(col, 2 * d.m);
+  if (val) d.val.download(val, 2 * d.m);
+  if (diag) d.diag.download(diag, d.n);
+  c.sync();
+}
+
+template <typename T>
+DVec<T> up(Ctx& c, const T* h, int64_t n) {
+  DVec<T> d(std::max<int64_t>(n, 1), c.s);
+  if (n && h) d.upload(h, n);
+  return d;
+}
+
+const DLevel& level_of(const lamg_hier* h, int32_t l) {
+  if (!h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null hierarchy");
+  if (l < 0 || l >= (int32_t)h->h->levels.size()) throw LamgError(LAMG_E_ARGUMENT, "level out of range");
+  return *h->h->levels[l];
+}
+
+// stage arrays given as host pointers -> device stage (for the transfer kernels)
+void upload_stage(Ctx& c, int32_t parent_n, int32_t coarse_n, int32_t nf, const int32_t* f_nodes,
+                  const double* f_diag, const int64_t* f_ptr, const int32_t* f_nbr, const double* f_val,
+                  const int32_t* cop, const int32_t* poc, DStage& s) {
+  s.parent_n = parent_n;
+  s.coarse_n = coarse_n;
+  s.nf = nf;
+  s.nnzf = f_ptr[nf];
+  s.f_nodes = up(c, f_nodes, nf);
+  s.f_diag = up(c, f_diag, nf);
+  s.f_ptr = up(c, f_ptr, nf + 1);
+  s.f_nbr = up(c, f_nbr, s.nnzf);
+  s.f_val = up(c, f_val, s.nnzf);
+  s.cop = up(c, cop, parent_n);
+  s.poc = up(c, poc, coarse_n);
+  build_stage_transpose(c, coarse_n, nf, s.f_ptr.p, s.f_nbr.p, s.cop.p, s.nnzf, s.t_ptr, s.t_p, s.f_of_p);
+}
+
+int solve_common(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, bool dev,
+                 const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
+                 int32_t cap) {
+  SolveResult res;
+  int rc = guarded([&] {
+    if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    Ctx& c = ctx->c;
+    set_device(c);
+    const int64_t n = h->h->levels[0]->op.n;
+    CycleCfg cc;
+    if (cfg) {
+      cc.correction = cfg->correction;
+      cc.mu = cfg->mu;
+      cc.max_cycles = cfg->max_cycles;
+      cc.target_reduction = cfg->target_reduction;
+      cc.divergence_factor = cfg->divergence_factor;
+    }
+    int r;
+    if (dev) {
+      r = solve_device(c, *h->h, b, x0, cc, x, res);
+    } else {
+      DVec<double> db(n, c.s), dx0(n, c.s), dx(n, c.s);
+      db.upload(b, n);
+      dx0.upload(x0, n);
+      r = solve_device(c, *h->h, db.p, dx0.p, cc, dx.p, res);
+      dx.download(x, n);
+      c.sync();
+    }
+    if (r != LAMG_OK) throw LamgError(r, res.message);
+  });
+  if (stats) {
+    stats->acf = res.acf;
+    stats->solve_work = res.solve_work;
+    stats->cycles = res.cycles;
+    stats->converged = res.converged ? 1 : 0;
+    stats->recombinations = res.recombinations;
+    stats->recomb_max_growth = res.recomb_max_growth;
+    stats->nresiduals = (int32_t)res.residuals.size();
+    stats->relax_sweeps = res.relax_sweeps;
+  }
+  if (residuals)
+    for (int32_t i = 0; i < cap && i < (int32_t)res.residuals.size(); ++i) residuals[i] = res.residuals[i];
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lamg_last_error(void) { return g_err.c_str(); }
+const char* lamg_version(void) { return "lamg_b200 0.1 (sm_100a)"; }
+
+int lamg_ctx_create(int device, int mode, lamg_ctx** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto* x = new lamg_ctx();
+    Ctx& c = x->c;
+    c.device = device;
+    c.mode = mode;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      delete x;
+      throw LamgError(LAMG_E_CUDA, "no CUDA device available (liblamg_b200 has no CPU path)");
+    }
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+    CK(cudaMalloc(&c.derr, sizeof(DevErr)));
+    CK(cudaMallocHost(&c.herr, sizeof(DevErr)));
+    CK(cudaMallocHost(&c.hscal, 64 * sizeof(double)));
+    CK(cudaMalloc(&c.dflag, 64 * sizeof(int)));
+    CK(cudaMalloc(&c.dscal, 256 * sizeof(double)));
+    CK(cudaMalloc(&c.dpart, 256 * sizeof(double)));
+    c.clear_err();
+    *out = x;
+  });
+}
+
+int lamg_ctx_set_mode(lamg_ctx* ctx, int mode) {
+  return guarded([&] {
+    if (mode != LAMG_MODE_VALIDATE && mode != LAMG_MODE_THROUGHPUT) throw LamgError(LAMG_E_ARGUMENT, "bad mode");
+    ctx->c.mode = mode;
+  });
+}
+
+void lamg_ctx_destroy(lamg_ctx* ctx) {
+  if (!ctx) return;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.s);
+  delete c.ws;
+  c.ws = nullptr;
+  c.res_csr = DCSR();
+  c.res_stage.f_diag.release();
+  c.res_stage.f_ptr.release();
+  c.res_stage.f_nbr.release();
+  c.res_stage.f_val.release();
+  c.res_stage.cop.release();
+  for (auto& v : c.prof.ev)
+    for (auto e : v) cudaEventDestroy(e);
+  cudaStreamSynchronize(c.s);
+  cudaFree(c.derr);
+  cudaFreeHost(c.herr);
+  cudaFreeHost(c.hscal);
+  cudaFree(c.dflag);
+  cudaFree(c.dscal);
+  cudaFree(c.dpart);
+  cudaStreamDestroy(c.s);
+  delete ctx;
+}
+
+// ------------------------------------------------------------------ setup
+int lamg_setup(lamg_ctx* ctx, const lamg_csr* a, int on_device, const lamg_setup_opts* opts,
+               lamg_hier** out) {
+  *out = nullptr;
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    SetupOpts o;
+    if (opts) {
+      o.gamma = opts->gamma;
+      o.seed = opts->rng_seed;
+      o.coarsest_n = opts->coarsest_n;
+      o.tv_sweeps = opts->tv_sweeps;
+      o.tv_count_finest = opts->tv_count_finest;
+      o.tv_count_max = opts->tv_count_max;
+    }
+    if (a->n <= 0) throw LamgError(LAMG_E_INVALID_LAPLACIAN, "empty matrix");
+    auto* h = new lamg_hier();
+    try {
+      if (on_device) {
+        CSRv v{a->n, a->m, a->row_ptr, a->col, a->val, a->diag};
+        h->h = setup_device(c, v, o);
+      } else {
+        DCSR d;
+        upload_csr(c, a, d);
+        h->h = setup_device(c, d.view(), o);
+      }
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    h->h->owner_stream = c.s;
+    *out = h;
+  });
+}
+
+void lamg_hier_destroy(lamg_hier* h) {
+  if (!h) return;
+  if (h->h) {
+    cudaSetDevice(h->h->device);
+    cudaDeviceSynchronize();
+  }
+  delete h;
+}
+
+int lamg_hier_info(const lamg_hier* h, int32_t* nlevels, double* setup_work, int32_t* nwarnings,
+                   double* setup_seconds) {
+  return guarded([&] {
+    if (!h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null hierarchy");
+    if (nlevels) *nlevels = (int32_t)h->h->levels.size();
+    if (setup_work) *setup_work = h->h->setup_work;
+    if (nwarnings) *nwarnings = (int32_t)h->h->warnings.size();
+    if (setup_seconds) *setup_seconds = h->h->setup_seconds;
+  });
+}
+
+int lamg_hier_warning(const lamg_hier* h, int32_t i, char* buf, int32_t cap) {
+  return guarded([&] {
+    if (!h || i < 0 || i >= (int32_t)h->h->warnings.size()) throw LamgError(LAMG_E_ARGUMENT, "bad warning index");
+    snprintf(buf, (size_t)cap, "%s", h->h->warnings[i].c_str());
+  });
+}
+
+int lamg_hier_level_info(const lamg_hier* h, int32_t l, lamg_level_info* o) {
+  return guarded([&] {
+    const DLevel& L = level_of(h, l);
+    memset(o, 0, sizeof *o);
+    o->kind = L.kind;
+    o->n = L.op.n;
+    o->m = L.op.m;
+    o->gamma = L.gamma;
+    o->nu_pre = L.nu_pre;
+    o->nu_post = L.nu_post;
+    o->tv_count = L.tv_count;
+    o->coarsest = L.coarsest;
+    o->nstages = (int32_t)L.stages.size();
+    o->dummy_aggregate = -1;
+    if (L.agg) {
+      o->coarse_n = L.agg->coarse_n;
+      o->alpha = L.agg->alpha;
+      o->stage_used = L.agg->stage_used;
+      o->dummy_aggregate = L.agg->dummy_aggregate;
+    }
+    o->gs_fronts = L.sched.nfronts;
+  });
+}
+
+int lamg_level_cycle_index(const lamg_hier* h, int32_t l, double gamma, double* out) {
+  return guarded([&] {
+    if (!h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null hierarchy");
+    *out = level_cycle_index(*h->h, (size_t)l, gamma);
+  });
+}
+
+int lamg_hier_download_op(const lamg_hier* h, int32_t l, int64_t* rp, int32_t* col, double* val,
+                          double* diag) {
+  return guarded([&] {
+    const DLevel& L = level_of(h, l);
+    CK(cudaSetDevice(h->h->device));
+    CK(cudaStreamSynchronize(h->h->owner_stream));
+    if (rp) CK(cudaMemcpy(rp, L.op.rp.p, sizeof(int64_t) * (L.op.n + 1), cudaMemcpyDeviceToHost));
+    if (col) CK(cudaMemcpy(col, L.op.col.p, sizeof(int32_t) * 2 * L.op.m, cudaMemcpyDeviceToHost));
+    if (val) CK(cudaMemcpy(val, L.op.val.p, sizeof(double) * 2 * L.op.m, cudaMemcpyDeviceToHost));
+    if (diag) CK(cudaMemcpy(diag, L.op.diag.p, sizeof(double) * L.op.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int lamg_hier_download_agg(const lamg_hier* h, int32_t l, int32_t* aggregate_of, int32_t* seed_of) {
+  return guarded([&] {
+    const DLevel& L = level_of(h, l);
+    if (!L.agg) throw LamgError(LAMG_E_ARGUMENT, "level is not an aggregation level");
+    CK(cudaSetDevice(h->h->device));
+    CK(cudaStreamSynchronize(h->h->owner_stream));
+    if (aggregate_of)
+      CK(cudaMemcpy(aggregate_of, L.agg->aggregate_of.p, sizeof(int32_t) * L.agg->fine_n, cudaMemcpyDeviceToHost));
+    if (seed_of) CK(cudaMemcpy(seed_of, L.agg->seed_of.p, sizeof(int32_t) * L.agg->coarse_n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int lamg_hier_stage_info(const lamg_hier* h, int32_t l, int32_t s, int32_t* parent_n, int32_t* coarse_n,
+                         int32_t* nf, int64_t* nnz_f) {
+  return guarded([&] {
+    const DLevel& L = level_of(h, l);
+    if (s < 0 || s >= (int32_t)L.stages.size()) throw LamgError(LAMG_E_ARGUMENT, "stage out of range");
+    const DStage& st = *L.stages[s];
+    *parent_n = st.parent_n;
+    *coarse_n = st.coarse_n;
+    *nf = st.nf;
+    *nnz_f = st.nnzf;
+  });
+}
+
+int lamg_hier_download_stage(const lamg_hier* h, int32_t l, int32_t s, int32_t* f_nodes, double* f_diag,
+                             int64_t* f_ptr, int32_t* f_nbr, double* f_val, int32_t* cop, int32_t* poc) {
+  return guarded([&] {
+    const DLevel& L = level_of(h, l);
+    if (s < 0 || s >= (int32_t)L.stages.size()) throw LamgError(LAMG_E_ARGUMENT, "stage out of range");
+    const DStage& st = *L.stages[s];
+    CK(cudaSetDevice(h->h->device));
+    CK(cudaStreamSynchronize(h->h->owner_stream));
+    auto cp = [](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    };
+    cp(f_nodes, st.f_nodes.p, sizeof(int32_t) * st.nf);
+    cp(f_diag, st.f_diag.p, sizeof(double) * st.nf);
+    cp(f_ptr, st.f_ptr.p, sizeof(int64_t) * (st.nf + 1));
+    cp(f_nbr, st.f_nbr.p, sizeof(int32_t) * st.nnzf);
+    cp(f_val, st.f_val.p, sizeof(double) * st.nnzf);
+    cp(cop, st.cop.p, sizeof(int32_t) * st.parent_n);
+    cp(poc, st.poc.p, sizeof(int32_t) * st.coarse_n);
+  });
+}
+
+// ------------------------------------------------------------------ solve
+int lamg_solve(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, const lamg_cycle_cfg* cfg,
+               double* x, lamg_solve_stats* stats, double* residuals, int32_t cap) {
+  return solve_common(ctx, h, b, x0, false, cfg, x, stats, residuals, cap);
+}
+
+int lamg_solve_dev(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, const lamg_cycle_cfg* cfg,
+                   double* x, lamg_solve_stats* stats, double* residuals, int32_t cap) {
+  return solve_common(ctx, h, b, x0, true, cfg, x, stats, residuals, cap);
+}
+
+int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {
+  return guarded([&] {
+    (void)ctx;
+    (void)h;
+  });
+}
+
+// -------------------------------------------------------------- profiling
+int lamg_ctx_profile(lamg_ctx* ctx, int enable) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    c.prof.enabled = enable != 0;
+    c.prof.used[0] = c.prof.used[1] = 0;
+  });
+}
+
+int lamg_ctx_profile_read(lamg_ctx* ctx, int kernel, int64_t* launches, double* total_ms, double* bytes) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    if (kernel < 0 || kernel > 1) throw LamgError(LAMG_E_ARGUMENT, "kernel class 0 (gs) or 1 (residual)");
+    c.sync();
+    double tot = 0.0;
+    for (int64_t i = 0; i < c.prof.used[kernel]; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c.prof.ev[kernel][2 * i], c.prof.ev[kernel][2 * i + 1]));
+      tot += ms;
+    }
+    *launches = c.prof.used[kernel];
+    *total_ms = tot;
+    *bytes = c.prof.bytes[kernel];
+  });
+}
+
+// ------------------------------------------------------- per-kernel API
+#define WITH_CSR(ctx, a)        \
+  Ctx& c = (ctx)->c;            \
+  set_device(c);                \
+  DCSR A_;                      \
+  upload_csr(c, a, A_);         \
+  const CSRv av = A_.view();
+
+int lamg_k_validate(lamg_ctx* ctx, const lamg_csr* a) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    validate_exact(c, av);
+  });
+}
+
+int lamg_k_mvm(lamg_ctx* ctx, const lamg_csr* a, const double* x, double* y) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto dx = up(c, x, a->n);
+    DVec<double> dy(std::max(a->n, 1), c.s);
+    residual_exact(c, av, nullptr, dx.p, dy.p);
+    dy.download(y, a->n);
+    c.sync();
+  });
+}
+
+int lamg_k_residual(lamg_ctx* ctx, const lamg_csr* a, const double* b, const double* x, double* r) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto dx = up(c, x, a->n);
+    auto db = up(c, b, a->n);
+    DVec<double> dr(std::max(a->n, 1), c.s);
+    residual_exact(c, av, db.p, dx.p, dr.p);
+    dr.download(r, a->n);
+    c.sync();
+  });
+}
+
+int lamg_k_energy(lamg_ctx* ctx, const lamg_csr* a, const double* x, double* e) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto dx = up(c, x, a->n);
+    UpperIndex upi;
+    build_upper_index(c, av, upi);
+    DVec<double> scratch;
+    energy_seq(c, av, upi, dx.p, c.dscal + 160, scratch);
+    *e = read_scalar(c, c.dscal + 160);
+  });
+}
+
+int lamg_k_gs_sweep(lamg_ctx* ctx, const lamg_csr* a, const double* b, double* x, int backward) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto dx = up(c, x, a->n);
+    DVec<double> db;
+    if (b) db = up(c, b, a->n);
+    Schedule sch;
+    build_schedule(c, av, backward != 0, sch);
+    gs_exact(c, av, sch, b ? db.p : nullptr, dx.p, 1, 1, backward != 0, true);
+    dx.download(x, a->n);
+    c.sync();
+  });
+}
+
+int lamg_k_generate_tvs(lamg_ctx* ctx, const lamg_csr* a, int32_t count, int32_t sweeps, uint64_t seed,
+                        double* out) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    Schedule sch;
+    build_schedule(c, av, false, sch);
+    DVec<double> X;
+    generate_tvs(c, av, sch, count, sweeps, seed, X);
+    std::vector<double> h = X.to_host();
+    for (int32_t k = 0; k < count; ++k)
+      for (int32_t u = 0; u < a->n; ++u) out[(int64_t)k * a->n + u] = h[(int64_t)u * count + k];
+  });
+}
+
+int lamg_k_probe(lamg_ctx* ctx, const lamg_csr* a, int32_t sweeps, uint64_t seed, double* factor) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    Schedule sch;
+    build_schedule(c, av, false, sch);
+    UpperIndex upi;
+    build_upper_index(c, av, upi);
+    *factor = probe_relaxation(c, av, sch, upi, sweeps, seed);
+  });
+}
+
+static DVec<double> upload_tvs_node_major(Ctx& c, int32_t n, int32_t K, const double* tvs) {
+  std::vector<double> h((size_t)n * K);
+  for (int32_t k = 0; k < K; ++k)
+    for (int32_t u = 0; u < n; ++u) h[(size_t)u * K + k] = tvs[(int64_t)k * n + u];
+  return up(c, h.data(), (int64_t)n * K);
+}
+
+int lamg_k_affinities(lamg_ctx* ctx, const lamg_csr* a, int32_t K, const double* tvs, double* aff,
+                      double* nn, int32_t* degenerate, int32_t* ndeg) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto X = upload_tvs_node_major(c, a->n, K, tvs);
+    DVec<double> daff(std::max<int64_t>(2 * a->m, 1), c.s), dnn(std::max(a->n, 1), c.s);
+    compute_affinities(c, av, K, X.p, daff.p, dnn.p);
+    daff.download(aff, 2 * a->m);
+    std::vector<double> hn(a->n);
+    dnn.download(hn.data(), a->n);
+    c.sync();
+    if (nn) memcpy(nn, hn.data(), sizeof(double) * a->n);
+    int32_t nd = 0;
+    for (int32_t u = 0; u < a->n; ++u)
+      if (hn[u] == 0.0) {
+        if (degenerate) degenerate[nd] = u;
+        ++nd;
+      }
+    if (ndeg) *ndeg = nd;
+  });
+}
+
+int lamg_k_detect_hubs(lamg_ctx* ctx, const lamg_csr* a, int32_t* hubs, int32_t* nhubs) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    DVec<int32_t> dh;
+    int32_t nh = detect_hubs(c, av, dh);
+    if (nh) dh.download(hubs, nh);
+    c.sync();
+    *nhubs = nh;
+  });
+}
+
+int lamg_k_aggregate(lamg_ctx* ctx, const lamg_csr* a, int32_t K, const double* tvs, double gamma,
+                     const int32_t* hubs, int32_t nhubs, int32_t* aggregate_of, int32_t* seed_of,
+                     int32_t* coarse_n, double* alpha, int32_t* stage_used, int32_t* dummy_aggregate) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto X = upload_tvs_node_major(c, a->n, K, tvs);
+    auto dh = up(c, hubs, nhubs);
+    DAgg t;
+    int stages = 1;
+    aggregate(c, av, K, X.p, gamma, dh.p, nhubs, t, &stages);
+    t.aggregate_of.download(aggregate_of, a->n);
+    if (seed_of && t.coarse_n) t.seed_of.download(seed_of, t.coarse_n);
+    c.sync();
+    *coarse_n = t.coarse_n;
+    *alpha = t.alpha;
+    *stage_used = t.stage_used;
+    *dummy_aggregate = t.dummy_aggregate;
+  });
+}
+
+int lamg_k_galerkin(lamg_ctx* ctx, const lamg_csr* a, const int32_t* aggregate_of, int32_t coarse_n) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto dagg = up(c, aggregate_of, a->n);
+    galerkin(c, av, dagg.p, coarse_n, c.res_csr);
+    c.res_stage.nf = 0;
+    c.sync();
+  });
+}
+
+int lamg_k_select_low_degree(lamg_ctx* ctx, const lamg_csr* a, int32_t max_degree, int32_t* f, int32_t* nf,
+                             int32_t* cc, int32_t* nc) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    SelectResult r;
+    select_low_degree(c, av, max_degree, r);
+    if (r.nf) r.f.download(f, r.nf);
+    if (r.nc) r.c.download(cc, r.nc);
+    c.sync();
+    *nf = r.nf;
+    *nc = r.nc;
+  });
+}
+
+int lamg_k_schur(lamg_ctx* ctx, const lamg_csr* a, const int32_t* f, int32_t nf, const int32_t* cset, int32_t nc,
+                 int32_t* unused) {
+  (void)unused;
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    auto df = up(c, f, nf);
+    auto dc = up(c, cset, nc);
+    DStage st;
+    schur_reduce(c, av, df.p, nf, dc.p, nc, st, c.res_csr, true);
+    c.res_stage.nf = nf;
+    c.res_stage.f_diag = std::move(st.f_diag);
+    c.res_stage.f_ptr = std::move(st.f_ptr);
+    c.res_stage.f_nbr = std::move(st.f_nbr);
+    c.res_stage.f_val = std::move(st.f_val);
+    c.res_stage.cop = std::move(st.cop);
+    c.sync();
+  });
+}
+
+int lamg_k_result_dims(lamg_ctx* ctx, int32_t* n, int64_t* m, int64_t* nnz_f) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    *n = c.res_csr.n;
+    *m = c.res_csr.m;
+    *nnz_f = c.res_stage.nf ? read_i64(c, c.res_stage.f_ptr.p + c.res_stage.nf) : 0;
+  });
+}
+
+int lamg_k_take_csr(lamg_ctx* ctx, int64_t* rp, int32_t* col, double* val, double* diag) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    download_csr(c, c.res_csr, rp, col, val, diag);
+  });
+}
+
+int lamg_k_take_stage(lamg_ctx* ctx, double* f_diag, int64_t* f_ptr, int32_t* f_nbr, double* f_val, int32_t* cop) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    auto& s = c.res_stage;
+    int64_t nnz = s.nf ? read_i64(c, s.f_ptr.p + s.nf) : 0;
+    if (s.nf) {
+      s.f_diag.download(f_diag, s.nf);
+      s.f_ptr.download(f_ptr, s.nf + 1);
+    } else if (f_ptr) {
+      f_ptr[0] = 0;
+    }
+    if (nnz) {
+      s.f_nbr.download(f_nbr, nnz);
+      s.f_val.download(f_val, nnz);
+    }
+    if (cop && s.cop.n) s.cop.download(cop, s.cop.n);
+    c.sync();
+  });
+}
+
+int lamg_k_restrict(lamg_ctx* ctx, const int32_t* agg, int32_t fine_n, int32_t coarse_n, const double* r,
+                    double* rc) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    auto da = up(c, agg, fine_n);
+    auto dr = up(c, r, fine_n);
+    DVec<int64_t> mp;
+    DVec<int32_t> mem;
+    build_members(c, fine_n, coarse_n, da.p, mp, mem);
+    DVec<double> drc(std::max(coarse_n, 1), c.s);
+    restrict_exact(c, coarse_n, mp.p, mem.p, dr.p, 1.0, drc.p);
+    drc.download(rc, coarse_n);
+    c.sync();
+  });
+}
+
+int lamg_k_interpolate(lamg_ctx* ctx, const int32_t* agg, int32_t fine_n, int32_t coarse_n, const double* ec,
+                       double* x) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    auto da = up(c, agg, fine_n);
+    auto de = up(c, ec, coarse_n);
+    auto dx = up(c, x, fine_n);
+    interpolate(c, fine_n, da.p, de.p, dx.p);
+    dx.download(x, fine_n);
+    c.sync();
+  });
+}
+
+int lamg_k_coarsen_rhs(lamg_ctx* ctx, int32_t parent_n, int32_t coarse_n, int32_t nf, const int32_t* f_nodes,
+                       const double* f_diag, const int64_t* f_ptr, const int32_t* f_nbr, const double* f_val,
+                       const int32_t* cop, const int32_t* poc, const double* b, double* bc) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    DStage s;
+    upload_stage(c, parent_n, coarse_n, nf, f_nodes, f_diag, f_ptr, f_nbr, f_val, cop, poc, s);
+    auto db = up(c, b, parent_n);
+    DVec<double> dbc(std::max(coarse_n, 1), c.s);
+    coarsen_rhs(c, s.view(), db.p, dbc.p);
+    dbc.download(bc, coarse_n);
+    c.sync();
+  });
+}
+
+int lamg_k_backsub(lamg_ctx* ctx, int32_t parent_n, int32_t coarse_n, int32_t nf, const int32_t* f_nodes,
+                   const double* f_diag, const int64_t* f_ptr, const int32_t* f_nbr, const double* f_val,
+                   const int32_t* cop, const int32_t* poc, const double* xc, const double* b, double* x) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    DStage s;
+    upload_stage(c, parent_n, coarse_n, nf, f_nodes, f_diag, f_ptr, f_nbr, f_val, cop, poc, s);
+    auto dxc = up(c, xc, coarse_n);
+    auto db = up(c, b, parent_n);
+    DVec<double> dx(std::max(parent_n, 1), c.s);
+    dx.zero();
+    backsub(c, s.view(), dxc.p, db.p, dx.p);
+    dx.download(x, parent_n);
+    c.sync();
+  });
+}
+
+int lamg_k_coarsest_direct(lamg_ctx* ctx, const lamg_csr* a, const double* b, double* x) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    DDirect d;
+    make_direct(c, av, d);
+    auto db = up(c, b, a->n);
+    auto dx = up(c, x, a->n);
+    DVec<double> scratch(2 * (int64_t)d.maxN + 2, c.s);
+    direct_solve(c, d, db.p, dx.p, true, scratch.p);
+    dx.download(x, a->n);
+    c.sync();
+  });
+}
+
+int lamg_k_coarsest_relax(lamg_ctx* ctx, const lamg_csr* a, const double* b, double* x) {
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    Schedule sch;
+    build_schedule(c, av, false, sch);
+    auto db = up(c, b, a->n);
+    auto dx = up(c, x, a->n);
+    DVec<double> r;
+    int sw = 0;
+    relax_solve(c, av, sch, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
+    dx.download(x, a->n);
+    c.sync();
+  });
+}
+
+int lamg_k_recombine(lamg_ctx* ctx, const lamg_csr* a, const double* b, int32_t cols, const double* saved_x,
+                     const double* saved_r, double* x, double* before, double* after) {
+  return guarded([&] {
+    if (cols < 1 || cols > 2) throw LamgError(LAMG_E_ERROR, "recombine supports one or two columns");
+    WITH_CSR(ctx, a);
+    const int64_t n = a->n;
+    auto db = up(c, b, n);
+    auto dx = up(c, x, n);
+    LevelWS w;
+    w.r.alloc(n, c.s);
+    w.tmp.alloc(n, c.s);
+    for (int i = 0; i < cols; ++i) {
+      w.saved_x[i] = up(c, saved_x + i * n, n);
+      w.saved_r[i] = up(c, saved_r + i * n, n);
+    }
+    double* growth = c.dscal + 170;
+    CK(cudaMemsetAsync(growth, 0, sizeof(double), c.s));
+    recombine_api(c, av, db.p, cols, w, dx.p, c.mode == LAMG_MODE_VALIDATE, growth);
+    dx.download(x, n);
+    CK(cudaMemcpyAsync(c.hscal, c.dscal + 120, 7 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    *before = std::sqrt(c.hscal[0]);
+    double nn = c.hscal[6];
+    *after = std::sqrt(nn < 0.0 ? 0.0 : nn);
+  });
+}
+
+int lamg_credit_takes(double gamma, int32_t count, int32_t* out) {
+  LevelCredits cr;
+  for (int32_t i = 0; i < count; ++i) out[i] = cr.take(0, gamma);
+  return LAMG_OK;
+}
+
+double lamg_flat_mu(double q) { return 2.0 * q / (q + 1.0); }
+
+uint64_t lamg_rng_derive(uint64_t seed, uint64_t stream) { return rng_derive_host(seed, stream); }
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+// common.cu -- context, error mapping, CUB wrappers and the bit-exact folds.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+
+namespace lamgb {
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), file, line, what);
+  throw LamgError(LAMG_E_CUDA, buf);
+}
+
+int Ctx::max_coop_blocks(const void* kernel, int threads, size_t smem) const {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * sms;
+}
+
+void Ctx::clear_err() {
+  DevErr e{~0ull, 0, 0, 0, 0, 0.0};
+  CK(cudaMemcpyAsync(derr, &e, sizeof e, cudaMemcpyHostToDevice, s));
+}
+
+unsigned long long Ctx::herr_key() {
+  CK(cudaMemcpyAsync(herr, derr, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
+  sync();
+  return herr->key;
+}
+
+void Ctx::set_err_phase(int ph) {
+  CK(cudaMemcpyAsync(&derr->phase, &ph, sizeof(int), cudaMemcpyHostToDevice, s));
+  sync();
+}
+
+// The reference's exception type and message for each device error kind.
+void Ctx::fetch_err_and_throw() {
+  CK(cudaMemcpyAsync(herr, derr, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
+  sync();
+  const DevErr& e = *herr;
+  char buf[256];
+  int code = LAMG_E_ERROR;
+  switch (e.code) {
+    case DE_GS_SINGULAR:
+      code = LAMG_E_SINGULAR_DIAGONAL;
+      snprintf(buf, sizeof buf, "zero diagonal at node %d", e.a);
+      break;
+    case DE_VAL_SELF:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "self entry stored in row %d", e.a);
+      break;
+    case DE_VAL_RANGE:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "column out of range");
+      break;
+    case DE_VAL_SORT:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "row %d not strictly sorted", e.a);
+      break;
+    case DE_VAL_STRUCT:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "structural asymmetry at (%d,%d)", e.a, e.b);
+      break;
+    case DE_VAL_VALUE:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "value asymmetry at (%d,%d)", e.a, e.b);
+      break;
+    case DE_VAL_ROWSUM:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "row %d sum %f exceeds tolerance", e.a, e.v);
+      break;
+    case DE_VAL_DIAG:
+      code = LAMG_E_INVALID_LAPLACIAN;
+      snprintf(buf, sizeof buf, "non-positive diagonal at non-isolated node %d", e.a);
+      break;
+    case DE_SCHUR_OVERLAP:
+      snprintf(buf, sizeof buf, "schur_reduce: F and C overlap at node %d", e.a);
+      break;
+    case DE_SCHUR_PIVOT:
+      code = LAMG_E_SINGULAR_DIAGONAL;
+      snprintf(buf, sizeof buf, "schur_reduce: non-positive pivot at node %d", e.a);
+      break;
+    case DE_SCHUR_DEPENDENT:
+      snprintf(buf, sizeof buf, "schur_reduce: F is not independent, edge (%d,%d)", e.a, e.b);
+      break;
+    default:
+      snprintf(buf, sizeof buf, "device error kind %d", e.code);
+  }
+  throw LamgError(code, buf);
+}
+
+void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** args, size_t smem) {
+  if (blocks < 1) blocks = 1;
+  CK(cudaLaunchCooperativeKernel(kernel, dim3(blocks), dim3(threads), args, smem, c.s));
+}
+
+// ------------------------------------------------------------- CUB wrappers
+namespace {
+struct Temp {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s;
+  explicit Temp(cudaStream_t st) : s(st) {}
+  void* get(size_t b) {
+    bytes = b;
+    if (b) CK(cudaMallocAsync(&p, b, s));
+    return p;
+  }
+  ~Temp() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+}  // namespace
+
+#define CUB_TWICE(call)                 \
+  do {                                  \
+    size_t bytes_ = 0;                  \
+    void* tmp_ = nullptr;               \
+    CK(call);                           \
+    Temp t_(c.s);                       \
+    tmp_ = t_.get(bytes_);              \
+    CK(call);                           \
+  } while (0)
+
+void sort_pairs_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, const int64_t* vin, int64_t* vout,
+                    int64_t n, int bits) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceRadixSort::SortPairs(tmp_, bytes_, kin, kout, vin, vout, (size_t)n, 0, bits, c.s));
+}
+void sort_pairs_u64_d(Ctx& c, const uint64_t* kin, uint64_t* kout, const double* vin, double* vout,
+                      int64_t n, int bits) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceRadixSort::SortPairs(tmp_, bytes_, kin, kout, vin, vout, (size_t)n, 0, bits, c.s));
+}
+void sort_pairs_u32_i32(Ctx& c, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                        int32_t* vout, int64_t n, int bits) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceRadixSort::SortPairs(tmp_, bytes_, kin, kout, vin, vout, (size_t)n, 0, bits, c.s));
+}
+void sort_pairs_u64_i32(Ctx& c, const uint64_t* kin, uint64_t* kout, const int32_t* vin,
+                        int32_t* vout, int64_t n, int bits) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceRadixSort::SortPairs(tmp_, bytes_, kin, kout, vin, vout, (size_t)n, 0, bits, c.s));
+}
+void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceScan::ExclusiveSum(tmp_, bytes_, in, out, n, c.s));
+}
+void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceScan::ExclusiveSum(tmp_, bytes_, in, out, n, c.s));
+}
+
+int64_t select_flagged_index(Ctx& c, const uint8_t* flags, int32_t* out, int64_t n) {
+  if (n <= 0) return 0;
+  int64_t* dcount = (int64_t*)c.dflag;
+  cub::CountingInputIterator<int32_t> it(0);
+  CUB_TWICE(cub::DeviceSelect::Flagged(tmp_, bytes_, it, flags, out, dcount, n, c.s));
+  return read_i64(c, dcount);
+}
+int64_t select_flagged_index64(Ctx& c, const uint8_t* flags, int64_t* out, int64_t n) {
+  if (n <= 0) return 0;
+  int64_t* dcount = (int64_t*)c.dflag;
+  cub::CountingInputIterator<int64_t> it(0);
+  CUB_TWICE(cub::DeviceSelect::Flagged(tmp_, bytes_, it, flags, out, dcount, n, c.s));
+  return read_i64(c, dcount);
+}
+
+double reduce_max_d(Ctx& c, const double* in, int64_t n) {
+  if (n <= 0) return 0.0;
+  double* d = c.dscal + 200;
+  CUB_TWICE(cub::DeviceReduce::Max(tmp_, bytes_, in, d, n, c.s));
+  return read_scalar(c, d);
+}
+int64_t reduce_sum_i64(Ctx& c, const int64_t* in, int64_t n) {
+  if (n <= 0) return 0;
+  int64_t* d = (int64_t*)(c.dscal + 201);
+  CUB_TWICE(cub::DeviceReduce::Sum(tmp_, bytes_, in, d, n, c.s));
+  return read_i64(c, d);
+}
+int32_t reduce_max_i32(Ctx& c, const int32_t* in, int64_t n) {
+  if (n <= 0) return 0;
+  int32_t* d = (int32_t*)(c.dscal + 202);
+  CUB_TWICE(cub::DeviceReduce::Max(tmp_, bytes_, in, d, n, c.s));
+  return read_i32(c, d);
+}
+
+double read_scalar(Ctx& c, const double* d) {
+  CK(cudaMemcpyAsync(c.hscal, d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  return c.hscal[0];
+}
+int64_t read_i64(Ctx& c, const int64_t* d) {
+  CK(cudaMemcpyAsync(c.hscal, d, sizeof(int64_t), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  int64_t v;
+  memcpy(&v, c.hscal, sizeof v);
+  return v;
+}
+int32_t read_i32(Ctx& c, const int32_t* d) {
+  CK(cudaMemcpyAsync(c.hscal, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  int32_t v;
+  memcpy(&v, c.hscal, sizeof v);
+  return v;
+}
+
+// ------------------------------------------------------- bit-exact folds
+// A left-to-right fold is one dependent chain of fp64 adds; one warp stages
+// the operands (coalesced 32-wide loads, 8 tiles in flight) and lane 0 runs
+// the chain from registers broadcast through shuffles.
+template <bool SQUARE>
+__global__ void seq_fold_kernel(const double* __restrict__ x, int64_t n, double* out) {
+  const int lane = threadIdx.x;
+  double s = 0.0;
+  constexpr int kTile = 32 * 8;
+  for (int64_t base = 0; base < n; base += kTile) {
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int64_t i = base + t * 32 + lane;
+      v[t] = i < n ? x[i] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int64_t rem = n - (base + t * 32);
+      int cnt = rem >= 32 ? 32 : (rem > 0 ? (int)rem : 0);
+      for (int j = 0; j < cnt; ++j) {
+        double y = __shfl_sync(0xffffffffu, v[t], j);
+        if (SQUARE) y = y * y;
+        s = s + y;
+      }
+    }
+  }
+  if (lane == 0) *out = SQUARE ? sqrt(s) : s;
+}
+
+void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
+  seq_fold_kernel<false><<<1, 32, 0, c.s>>>(x, n, d_out);
+  CK_LAUNCH();
+}
+void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
+  seq_fold_kernel<true><<<1, 32, 0, c.s>>>(x, n, d_out);
+  CK_LAUNCH();
+}
+
+// fixed-order two-level tree reduction: deterministic for a given n
+template <bool SQUARE>
+__global__ void tree_partial_kernel(const double* __restrict__ x, int64_t n, double* part) {
+  __shared__ double sh[kThreads];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = x[i];
+    s += SQUARE ? v * v : v;
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+template <bool SQUARE>
+__global__ void tree_final_kernel(const double* part, int np, double* out) {
+  __shared__ double sh[512];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = SQUARE ? sqrt(sh[0]) : sh[0];
+}
+
+void tree_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
+  double* part = c.dpart;
+  int nb = (int)std::min<int64_t>(256, blocks_for(n));
+  tree_partial_kernel<false><<<nb, kThreads, 0, c.s>>>(x, n, part);
+  tree_final_kernel<false><<<1, 256, 0, c.s>>>(part, nb, d_out);
+  CK_LAUNCH();
+}
+void tree_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
+  double* part = c.dpart;
+  int nb = (int)std::min<int64_t>(256, blocks_for(n));
+  tree_partial_kernel<true><<<nb, kThreads, 0, c.s>>>(x, n, part);
+  tree_final_kernel<true><<<1, 256, 0, c.s>>>(part, nb, d_out);
+  CK_LAUNCH();
+}
+
+}  // namespace lamgb

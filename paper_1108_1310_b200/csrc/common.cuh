@@ -1,0 +1,269 @@
+// common.cuh -- shared host/device infrastructure of liblamg_b200.
+//
+// Everything is compiled with --fmad=false: every fp64 multiply and add is
+// rounded separately, in source order, exactly as the reference's x86-64
+// build evaluates them, so kernels that keep the
+// reference's fold order are bit-identical to it.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lamg_b200.h"
+
+namespace lamgb {
+
+namespace cg = cooperative_groups;
+
+// ----------------------------------------------------------------- errors
+struct LamgError : std::runtime_error {
+  int code;
+  LamgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define CK(x)                                                    \
+  do {                                                           \
+    cudaError_t e_ = (x);                                        \
+    if (e_ != cudaSuccess) ::lamgb::cuda_fail(e_, #x, __FILE__, __LINE__); \
+  } while (0)
+#define CK_LAUNCH() CK(cudaGetLastError())
+
+// ------------------------------------------------------ device error slot
+// Kernels that can fail record the FIRST failure in the reference's
+// sequential order as a 64-bit ordering key (atomicMin). A failing kernel is
+// then re-run in "payload" phase, where only the thread(s) holding the
+// winning key write the payload (node ids, row sum) used to format the
+// reference's message. Kernels that report errors are therefore re-runnable
+// (read-only, or their output is discarded on error).
+struct DevErr {
+  unsigned long long key;  // ULLONG_MAX = none
+  int phase;               // 0 = find min key, 1 = write payload
+  int code;                // device error kind (errors.cu)
+  int a, b;
+  double v;
+};
+
+__device__ inline void dev_report(DevErr* e, unsigned long long key, int code, int a, int b,
+                                  double v = 0.0) {
+  if (e->phase == 0) {
+    atomicMin(&e->key, key);
+  } else if (key == e->key) {
+    e->code = code;
+    e->a = a;
+    e->b = b;
+    e->v = v;
+  }
+}
+
+// device error kinds -> (status, message) in errors.cu
+enum DevErrKind {
+  DE_GS_SINGULAR = 1,  // smoothing.cpp:17-23
+  DE_VAL_SELF,         // sparse_laplacian.cpp:206
+  DE_VAL_RANGE,        // :207
+  DE_VAL_SORT,         // :208-210
+  DE_VAL_STRUCT,       // :214-217
+  DE_VAL_VALUE,        // :219-222
+  DE_VAL_ROWSUM,       // :225-228
+  DE_VAL_DIAG,         // :229-232
+  DE_SCHUR_OVERLAP,    // elimination.cpp:42-44
+  DE_SCHUR_PIVOT,      // :45-48
+  DE_SCHUR_DEPENDENT,  // :53-56
+};
+
+// ------------------------------------------------------------ device memory
+template <typename T>
+struct DVec {
+  T* p = nullptr;
+  int64_t n = 0;
+  cudaStream_t s = 0;
+  DVec() = default;
+  DVec(int64_t count, cudaStream_t st) { alloc(count, st); }
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  DVec(DVec&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DVec& operator=(DVec&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DVec() { release(); }
+  void alloc(int64_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count > 0) CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void zero() { if (n) CK(cudaMemsetAsync(p, 0, sizeof(T) * (size_t)n, s)); }
+  void fill_bytes(int byte) { if (n) CK(cudaMemsetAsync(p, byte, sizeof(T) * (size_t)n, s)); }
+  void upload(const T* h, int64_t count) {
+    if (count) CK(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, s));
+  }
+  void download(T* h, int64_t count) const {
+    if (count) CK(cudaMemcpyAsync(h, p, sizeof(T) * (size_t)count, cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<T> to_host() const {
+    std::vector<T> v((size_t)n);
+    download(v.data(), n);
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+  T* get() const { return p; }
+};
+
+// -------------------------------------------------------------- CSR views
+struct CSRv {  // device view of a lamg::SparseLaplacian
+  int32_t n = 0;
+  int64_t m = 0;
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+  const double* diag = nullptr;
+};
+
+struct DCSR {  // owning device CSR
+  int32_t n = 0;
+  int64_t m = 0;
+  DVec<int64_t> rp;
+  DVec<int32_t> col;
+  DVec<double> val;
+  DVec<double> diag;
+  CSRv view() const { return CSRv{n, m, rp.p, col.p, val.p, diag.p}; }
+  void alloc(int32_t nn, int64_t mm, cudaStream_t s) {
+    n = nn;
+    m = mm;
+    rp.alloc(nn + 1, s);
+    col.alloc(2 * mm, s);
+    val.alloc(2 * mm, s);
+    diag.alloc(nn, s);
+  }
+};
+
+// ---------------------------------------------------------------- context
+struct Workspace;  // solve.cuh
+
+struct Profile {
+  bool enabled = false;
+  std::vector<cudaEvent_t> ev[2];  // start/stop pairs per kernel class
+  int64_t used[2] = {0, 0};
+  double bytes[2] = {0, 0};
+};
+
+struct Ctx {
+  int device = 0;
+  int mode = LAMG_MODE_VALIDATE;
+  int sms = 148;
+  cudaStream_t s = nullptr;
+  DevErr* derr = nullptr;       // device error slot
+  DevErr* herr = nullptr;       // pinned mirror
+  double* hscal = nullptr;      // pinned scalar readback area (64 doubles)
+  int* dflag = nullptr;         // scratch device ints (64)
+  double* dscal = nullptr;      // scratch device scalars (256 doubles)
+  double* dpart = nullptr;      // tree-reduction partials (256 doubles)
+  double work = 0.0;            // thread-local work::total() equivalent (edge units)
+  Profile prof;
+  Workspace* ws = nullptr;      // solve workspace (owned; solve.cu)
+  // per-kernel API results kept until taken
+  DCSR res_csr;
+  struct {
+    int32_t nf = 0;
+    DVec<double> f_diag;
+    DVec<int64_t> f_ptr;
+    DVec<int32_t> f_nbr;
+    DVec<double> f_val;
+    DVec<int32_t> cop;
+  } res_stage;
+  int max_coop_blocks(const void* kernel, int threads, size_t smem = 0) const;
+  void clear_err();
+  // syncs; if a kernel recorded a failure, re-runs `launch` in payload phase
+  // and throws the reference's exception for it
+  template <typename F>
+  void checked(F&& launch) {
+    clear_err();
+    launch();
+    sync();
+    if (herr_key() != ~0ull) {
+      set_err_phase(1);
+      launch();
+      sync();
+      fetch_err_and_throw();
+    }
+  }
+  unsigned long long herr_key();
+  void set_err_phase(int ph);
+  [[noreturn]] void fetch_err_and_throw();
+  void sync() { CK(cudaStreamSynchronize(s)); }
+};
+
+
+// ---------------------------------------------------------- launch helpers
+constexpr int kThreads = 256;
+inline int blocks_for(int64_t n, int threads = kThreads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > (1 << 30)) b = 1 << 30;
+  return (int)b;
+}
+
+// grid barrier usable from cooperative kernels; one block uses __syncthreads
+__device__ inline void grid_barrier() {
+  if (gridDim.x == 1) {
+    __syncthreads();
+  } else {
+    cg::this_grid().sync();
+  }
+}
+
+// launches a kernel cooperatively (all blocks co-resident)
+void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** args, size_t smem = 0);
+
+// ------------------------------------------------------------- CUB wrappers
+// stable LSD radix sort of (key, value) pairs on the low `bits` key bits
+void sort_pairs_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, const int64_t* vin,
+                    int64_t* vout, int64_t n, int bits);
+void sort_pairs_u64_d(Ctx& c, const uint64_t* kin, uint64_t* kout, const double* vin,
+                      double* vout, int64_t n, int bits);
+void sort_pairs_u32_i32(Ctx& c, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                        int32_t* vout, int64_t n, int bits);
+void sort_pairs_u64_i32(Ctx& c, const uint64_t* kin, uint64_t* kout, const int32_t* vin,
+                        int32_t* vout, int64_t n, int bits);
+void exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n);
+void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n);
+// stable compaction of [0, n) indices where flag != 0; returns the count
+int64_t select_flagged_index(Ctx& c, const uint8_t* flags, int32_t* out, int64_t n);
+int64_t select_flagged_index64(Ctx& c, const uint8_t* flags, int64_t* out, int64_t n);
+double reduce_max_d(Ctx& c, const double* in, int64_t n);   // exact (max)
+int64_t reduce_sum_i64(Ctx& c, const int64_t* in, int64_t n);
+int32_t reduce_max_i32(Ctx& c, const int32_t* in, int64_t n);
+
+// --------------------------------------------------------- bit-exact folds
+// out = ((0 + x0) + x1) + ... (the reference's left-to-right fold); device result
+void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out);
+// out = sqrt(sum x_i^2) with the same fold order (norm2, sparse_laplacian.cpp:236-240)
+void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out);
+// fixed-order tree reductions (throughput mode)
+void tree_sum(Ctx& c, const double* x, int64_t n, double* d_out);
+void tree_norm2(Ctx& c, const double* x, int64_t n, double* d_out);
+
+// rounded-to-host scalar read (syncs)
+double read_scalar(Ctx& c, const double* d);
+int64_t read_i64(Ctx& c, const int64_t* d);
+int32_t read_i32(Ctx& c, const int32_t* d);
+
+}  // namespace lamgb

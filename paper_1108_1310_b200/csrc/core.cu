@@ -1,0 +1,504 @@
+// core.cu -- CSR residual, exact-order Gauss-Seidel, transfers, validation.
+//
+// Arithmetic follows the reference op-for-op (no FMA, left-to-right folds in
+// the reference's order) so every kernel here is bit-identical to it.
+#include <algorithm>
+#include <cmath>
+
+#include "core.cuh"
+
+namespace lamgb {
+
+// ------------------------------------------------------------- residual
+// thread per row; the row fold runs in column order (sparse_laplacian.cpp:156-160)
+__global__ void residual_exact_kernel(CSRv a, const double* __restrict__ b,
+                                      const double* __restrict__ x, double* __restrict__ r) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n) return;
+  double s = a.diag[u] * x[u];
+  const int64_t e = a.rp[u + 1];
+  for (int64_t k = a.rp[u]; k < e; ++k) s = s + a.val[k] * x[a.col[k]];
+  r[u] = b ? b[u] - s : s;
+}
+
+void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r) {
+  if (a.n == 0) return;
+  residual_exact_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, b, x, r);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------ GS wavefronts
+__global__ void deps_kernel(CSRv a, bool backward, int32_t* cnt) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n) return;
+  int32_t c = 0;
+  for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
+    int32_t v = a.col[k];
+    c += backward ? (v > u) : (v < u);
+  }
+  cnt[u] = c;
+}
+
+__global__ void zero_dep_flags_kernel(const int32_t* cnt, int32_t n, uint8_t* flag) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < n) flag[u] = cnt[u] == 0;
+}
+
+// Kahn's algorithm, one grid barrier per front: finishing a row releases its
+// later neighbours; a row joins the next front when its last earlier
+// neighbour finishes.
+__global__ void kahn_kernel(CSRv a, bool backward, int32_t* cnt, int32_t* level, int32_t* queue,
+                            int32_t* ctl /* [0]=tail, [1]=nfronts */, int32_t first_count) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  int32_t fs = 0, fe = first_count, r = 0;
+  while (fs < fe) {
+    for (int64_t i = fs + gtid; i < fe; i += gstride) {
+      int32_t u = queue[i];
+      level[u] = r;
+      for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
+        int32_t v = a.col[k];
+        bool later = backward ? (v < u) : (v > u);
+        if (later && atomicSub(&cnt[v], 1) == 1) queue[atomicAdd(&ctl[0], 1)] = v;
+      }
+    }
+    grid_barrier();
+    fs = fe;
+    fe = *(volatile int32_t*)&ctl[0];
+    ++r;
+    grid_barrier();
+  }
+  if (gtid == 0) ctl[1] = r;
+}
+
+__global__ void front_bounds_kernel(const uint32_t* lvl_sorted, int32_t n, int32_t* front_ptr,
+                                    int32_t nfronts) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0 || lvl_sorted[i] != lvl_sorted[i - 1]) front_ptr[lvl_sorted[i]] = i;
+  if (i == 0) front_ptr[nfronts] = n;
+}
+
+__global__ void iota_kernel(int32_t* x, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (int32_t)i;
+}
+
+void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
+  const int32_t n = a.n;
+  out.nfronts = 0;
+  out.max_width = 0;
+  if (n == 0) return;
+  DVec<int32_t> cnt(n, c.s), level(n, c.s), queue(n, c.s);
+  DVec<uint8_t> flag(n, c.s);
+  deps_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, backward, cnt.p);
+  zero_dep_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(cnt.p, n, flag.p);
+  CK_LAUNCH();
+  int32_t first = (int32_t)select_flagged_index(c, flag.p, queue.p, n);
+  int32_t* ctl = c.dflag + 8;
+  int32_t init[2] = {first, 0};
+  CK(cudaMemcpyAsync(ctl, init, sizeof init, cudaMemcpyHostToDevice, c.s));
+  const int threads = 256;
+  int blocks = std::min(c.max_coop_blocks((const void*)kahn_kernel, threads), blocks_for(n, threads));
+  if (n < 4096) blocks = 1;
+  CSRv av = a;
+  bool bw = backward;
+  void* args[] = {&av, &bw, &cnt.p, &level.p, &queue.p, &ctl, &first};
+  coop_launch(c, (const void*)kahn_kernel, blocks, threads, args);
+  int32_t nf = read_i32(c, ctl + 1);
+  // rows sorted by (front, row): stable radix sort of the identity by front
+  DVec<uint32_t> keys_out(n, c.s);
+  DVec<int32_t> ids(n, c.s);
+  iota_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
+  CK_LAUNCH();
+  out.rows.alloc(n, c.s);
+  int bits = 1;
+  while ((1u << bits) <= (uint32_t)nf && bits < 32) ++bits;
+  sort_pairs_u32_i32(c, (const uint32_t*)level.p, keys_out.p, ids.p, out.rows.p, n, bits);
+  out.front_ptr.alloc(nf + 1, c.s);
+  front_bounds_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(keys_out.p, n, out.front_ptr.p, nf);
+  CK_LAUNCH();
+  out.nfronts = nf;
+  std::vector<int32_t> fp = out.front_ptr.to_host();
+  int32_t w = 0;
+  for (int32_t f = 0; f < nf; ++f) w = std::max(w, fp[f + 1] - fp[f]);
+  out.max_width = w;
+}
+
+// One persistent launch per sweep set: rows of a front update in parallel,
+// a grid barrier separates fronts. K-wide rows reuse the row's column and
+// value loads for all K vectors.
+__global__ void gs_fronts_kernel(CSRv a, const double* __restrict__ b, double* x, int K,
+                                 const int32_t* __restrict__ front_ptr, const int32_t* __restrict__ rows,
+                                 int32_t nfronts, int sweeps, int backward, DevErr* err) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int32_t f = 0; f < nfronts; ++f) {
+      const int32_t fs = front_ptr[f], fe = front_ptr[f + 1];
+      for (int64_t i = fs + gtid / K; i < fe; i += gstride / K) {
+        const int kk = (int)(gtid % K);
+        const int32_t u = rows[i];
+        double s = b ? b[(int64_t)u * K + kk] : 0.0;
+        const int64_t e = a.rp[u + 1];
+        for (int64_t k = a.rp[u]; k < e; ++k) s = s - a.val[k] * x[(int64_t)a.col[k] * K + kk];
+        const double d = a.diag[u];
+        if (d == 0.0) {
+          if (e != a.rp[u])
+            dev_report(err, backward ? (unsigned long long)(a.n - 1 - u) : (unsigned long long)u,
+                       DE_GS_SINGULAR, u, 0);
+          continue;
+        }
+        x[(int64_t)u * K + kk] = s / d;
+      }
+      grid_barrier();
+    }
+  }
+}
+
+void gs_exact(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, double* x, int K,
+              int sweeps, bool backward, bool check) {
+  if (a.n == 0 || sweeps <= 0) return;
+  const int threads = 256;
+  int64_t work = (int64_t)sch.max_width * K;
+  int blocks = (int)std::min<int64_t>(c.max_coop_blocks((const void*)gs_fronts_kernel, threads),
+                                      std::max<int64_t>(1, (work + threads - 1) / threads));
+  // small fronts: a single CTA synchronises with __syncthreads only
+  if (work <= 2 * threads) blocks = 1;
+  CSRv av = a;
+  const int32_t* fp = sch.front_ptr.p;
+  const int32_t* rw = sch.rows.p;
+  int32_t nf = sch.nfronts;
+  int bw = backward ? 1 : 0;
+  int t = (threads / K) * K;  // (row, k) pairs tile the grid exactly
+  void* args[] = {&av, (void*)&b, &x, &K, (void*)&fp, (void*)&rw, &nf, &sweeps, &bw, &c.derr};
+  if (check) c.checked([&] { coop_launch(c, (const void*)gs_fronts_kernel, blocks, t, args); });
+  else coop_launch(c, (const void*)gs_fronts_kernel, blocks, t, args);
+}
+
+// ----------------------------------------------------------------- energy
+__global__ void upper_flags_kernel(CSRv a, uint8_t* flag, int32_t* row_of) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n) return;
+  for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
+    flag[k] = a.col[k] > u;
+    row_of[k] = u;
+  }
+}
+__global__ void gather_rows_kernel(const int64_t* entry, const int32_t* row_of, int64_t cnt,
+                                   int32_t* out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < cnt) out[j] = row_of[entry[j]];
+}
+
+void build_upper_index(Ctx& c, const CSRv& a, UpperIndex& out) {
+  const int64_t nnz = 2 * a.m;
+  out.entry.alloc(a.m, c.s);
+  out.row.alloc(a.m, c.s);
+  out.count = 0;
+  if (nnz == 0) return;
+  DVec<uint8_t> flag(nnz, c.s);
+  DVec<int32_t> row_of(nnz, c.s);
+  upper_flags_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, flag.p, row_of.p);
+  CK_LAUNCH();
+  out.count = select_flagged_index64(c, flag.p, out.entry.p, nnz);
+  gather_rows_kernel<<<blocks_for(out.count), kThreads, 0, c.s>>>(out.entry.p, row_of.p, out.count, out.row.p);
+  CK_LAUNCH();
+}
+
+__global__ void energy_terms_kernel(CSRv a, const int64_t* entry, const int32_t* row, int64_t cnt,
+                                    const double* __restrict__ x, double* t) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= cnt) return;
+  int64_t k = entry[j];
+  double d = x[row[j]] - x[a.col[k]];
+  t[j] = -a.val[k] * d * d;
+}
+
+void energy_seq(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, double* d_out,
+                DVec<double>& scratch) {
+  if (scratch.n < up.count) scratch.alloc(up.count, c.s);
+  if (up.count == 0) {
+    CK(cudaMemsetAsync(d_out, 0, sizeof(double), c.s));
+    return;
+  }
+  energy_terms_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, x, scratch.p);
+  CK_LAUNCH();
+  seq_sum(c, scratch.p, up.count, d_out);
+}
+
+// -------------------------------------------------------------------- rng
+__device__ inline uint64_t splitmix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__global__ void fill_pm1_kernel(double* x, int64_t n, uint64_t s0, int stride, int offset) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t state = s0 + (uint64_t)(i + 3) * 0x9e3779b97f4a7c15ULL;
+  double unit = (double)(splitmix(state) >> 11) * 0x1.0p-53;
+  x[i * stride + offset] = 2.0 * unit - 1.0;
+}
+void fill_pm1(Ctx& c, double* x, int64_t n, uint64_t seed, int stride, int offset) {
+  if (n == 0) return;
+  uint64_t s0 = seed ? seed : 0x9e3779b97f4a7c15ULL;
+  fill_pm1_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, s0, stride, offset);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------- mean subtraction
+// K columns folded independently, one lane per column, rows in order
+__global__ void col_seq_sum_kernel(const double* __restrict__ x, int64_t n, int K, double* sums) {
+  int k = threadIdx.x;
+  if (k >= K) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s = s + x[i * K + k];
+  sums[k] = s;
+}
+__global__ void sub_mean_kernel(double* x, int64_t n, int K, const double* sums) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * K) return;
+  int k = (int)(i % K);
+  double mean = sums[k] / (double)n;
+  x[i] = x[i] - mean;
+}
+
+void subtract_mean_seq(Ctx& c, double* x, int64_t n, int K) {
+  if (n == 0) return;
+  double* sums = c.dscal + 64;  // [64..80)
+  if (K == 1) seq_sum(c, x, n, sums);
+  else {
+    col_seq_sum_kernel<<<1, 32, 0, c.s>>>(x, n, K, sums);
+    CK_LAUNCH();
+  }
+  sub_mean_kernel<<<blocks_for(n * K), kThreads, 0, c.s>>>(x, n, K, sums);
+  CK_LAUNCH();
+}
+
+void subtract_mean_tree(Ctx& c, double* x, int64_t n) {
+  if (n == 0) return;
+  double* sums = c.dscal + 64;
+  tree_sum(c, x, n, sums);
+  sub_mean_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, 1, sums);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------------- validation
+__global__ void abs_max_kernel(const double* __restrict__ d, int32_t n, unsigned long long* out) {
+  __shared__ double sh[kThreads];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(d[i]));
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sh[0]));
+}
+
+__device__ inline unsigned long long vkey(int32_t u, int64_t pos, int sub) {
+  return ((unsigned long long)u << 32) | ((unsigned long long)pos << 3) | (unsigned long long)sub;
+}
+
+__global__ void validate_kernel(CSRv a, const unsigned long long* maxdiag_bits, DevErr* err) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n) return;
+  const double md = __longlong_as_double((long long)*maxdiag_bits);
+  const double tol = 1e-10 * (md < 1e-300 ? 1e-300 : md);
+  double row_sum = a.diag[u];
+  const int64_t b = a.rp[u], e = a.rp[u + 1];
+  for (int64_t k = b; k < e; ++k) {
+    const int32_t v = a.col[k];
+    const int64_t pos = k - b;
+    if (v == u) { dev_report(err, vkey(u, pos, 0), DE_VAL_SELF, u, v); return; }
+    if (v < 0 || v >= a.n) { dev_report(err, vkey(u, pos, 1), DE_VAL_RANGE, u, v); return; }
+    if (k > b && a.col[k - 1] >= v) { dev_report(err, vkey(u, pos, 2), DE_VAL_SORT, u, v); return; }
+    int64_t lo = a.rp[v], hi = a.rp[v + 1];
+    while (lo < hi) {
+      int64_t mid = lo + (hi - lo) / 2;
+      if (a.col[mid] < u) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo == a.rp[v + 1] || a.col[lo] != u) { dev_report(err, vkey(u, pos, 3), DE_VAL_STRUCT, u, v); return; }
+    if (a.val[lo] != a.val[k]) { dev_report(err, vkey(u, pos, 4), DE_VAL_VALUE, u, v); return; }
+    row_sum = row_sum + a.val[k];
+  }
+  if (fabs(row_sum) > tol) { dev_report(err, vkey(u, e - b, 5), DE_VAL_ROWSUM, u, 0, row_sum); return; }
+  if (e > b && a.diag[u] <= 0.0) dev_report(err, vkey(u, e - b, 6), DE_VAL_DIAG, u, 0);
+}
+
+void validate_exact(Ctx& c, const CSRv& a) {
+  if (a.n <= 0) throw LamgError(LAMG_E_INVALID_LAPLACIAN, "empty matrix");
+  unsigned long long* md = (unsigned long long*)(c.dscal + 90);
+  CK(cudaMemsetAsync(md, 0, sizeof(unsigned long long), c.s));
+  abs_max_kernel<<<std::min(blocks_for(a.n), 1024), kThreads, 0, c.s>>>(a.diag, a.n, md);
+  CK_LAUNCH();
+  c.checked([&] {
+    validate_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, md, c.derr);
+    CK_LAUNCH();
+  });
+}
+
+// -------------------------------------------------------------- transfers
+__global__ void restrict_kernel(int32_t cn, const int64_t* __restrict__ mem_ptr,
+                                const int32_t* __restrict__ mem, const double* __restrict__ r,
+                                double mu, double* __restrict__ rc) {
+  int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= cn) return;
+  double s = 0.0;
+  for (int64_t j = mem_ptr[g]; j < mem_ptr[g + 1]; ++j) s = s + r[mem[j]];
+  rc[g] = mu != 1.0 ? s * mu : s;
+}
+void restrict_exact(Ctx& c, int32_t coarse_n, const int64_t* mem_ptr, const int32_t* mem,
+                    const double* r, double mu, double* rc) {
+  if (coarse_n == 0) return;
+  restrict_kernel<<<blocks_for(coarse_n), kThreads, 0, c.s>>>(coarse_n, mem_ptr, mem, r, mu, rc);
+  CK_LAUNCH();
+}
+
+__global__ void interpolate_kernel(int32_t n, const int32_t* __restrict__ agg,
+                                   const double* __restrict__ ec, double* __restrict__ x) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < n) x[u] = x[u] + ec[agg[u]];
+}
+void interpolate(Ctx& c, int32_t fine_n, const int32_t* agg, const double* ec, double* x) {
+  if (fine_n == 0) return;
+  interpolate_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(fine_n, agg, ec, x);
+  CK_LAUNCH();
+}
+
+__global__ void coarsen_rhs_kernel(StageV s, const double* __restrict__ b, double* __restrict__ bc) {
+  int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= s.coarse_n) return;
+  double v = b[s.poc[k]];
+  for (int64_t j = s.t_ptr[k]; j < s.t_ptr[k + 1]; ++j) {
+    const int64_t p = s.t_p[j];
+    const int32_t i = s.f_of_p[p];
+    const double scaled = b[s.f_nodes[i]] / s.f_diag[i];
+    v = v - s.f_val[p] * scaled;
+  }
+  bc[k] = v;
+}
+void coarsen_rhs(Ctx& c, const StageV& s, const double* b, double* bc) {
+  if (s.coarse_n == 0) return;
+  coarsen_rhs_kernel<<<blocks_for(s.coarse_n), kThreads, 0, c.s>>>(s, b, bc);
+  CK_LAUNCH();
+}
+
+__global__ void gather_kernel(double* dst, const double* src, const int32_t* idx, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void scatter_kernel(double* dst, const double* src, const int32_t* idx, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+void gather_d(Ctx& c, double* dst, const double* src, const int32_t* idx, int64_t n) {
+  if (n == 0) return;
+  gather_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
+  CK_LAUNCH();
+}
+void scatter_d(Ctx& c, double* dst, const double* src, const int32_t* idx, int64_t n) {
+  if (n == 0) return;
+  scatter_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
+  CK_LAUNCH();
+}
+void copy_d(Ctx& c, double* dst, const double* src, int64_t n) {
+  if (n) CK(cudaMemcpyAsync(dst, src, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c.s));
+}
+
+void inject(Ctx& c, const StageV& s, const double* x, double* xc) { gather_d(c, xc, x, s.poc, s.coarse_n); }
+
+__global__ void backsub_f_kernel(StageV s, const double* __restrict__ b, double* x) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.nf) return;
+  const int32_t f = s.f_nodes[i];
+  double sum = b[f];
+  for (int64_t p = s.f_ptr[i]; p < s.f_ptr[i + 1]; ++p) sum = sum - s.f_val[p] * x[s.f_nbr[p]];
+  x[f] = sum / s.f_diag[i];
+}
+void backsub(Ctx& c, const StageV& s, const double* xc, const double* b, double* x) {
+  scatter_d(c, x, xc, s.poc, s.coarse_n);
+  if (s.nf == 0) return;
+  backsub_f_kernel<<<blocks_for(s.nf), kThreads, 0, c.s>>>(s, b, x);
+  CK_LAUNCH();
+}
+
+__global__ void stage_keys_kernel(int32_t nf, const int64_t* f_ptr, const int32_t* f_nbr,
+                                  const int32_t* cop, uint32_t* key, int32_t* f_of_p) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  for (int64_t p = f_ptr[i]; p < f_ptr[i + 1]; ++p) {
+    key[p] = (uint32_t)cop[f_nbr[p]];
+    f_of_p[p] = i;
+  }
+}
+__global__ void iota64_kernel(int64_t* x, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+__global__ void seg_bounds64_kernel(const uint64_t* sorted_key, int64_t n, int32_t nseg, int64_t* ptr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  uint64_t lo = i == 0 ? 0ull : sorted_key[i - 1] + 1ull;
+  uint64_t hi = i == n ? (uint64_t)nseg : sorted_key[i];
+  for (uint64_t k = lo; k <= hi && k <= (uint64_t)nseg; ++k) ptr[k] = i;
+}
+
+__global__ void widen_kernel(const uint32_t* in, int64_t n, uint64_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+void build_stage_transpose(Ctx& c, int32_t coarse_n, int32_t nf, const int64_t* f_ptr,
+                           const int32_t* f_nbr, const int32_t* cop, int64_t nnzf,
+                           DVec<int64_t>& t_ptr, DVec<int64_t>& t_p, DVec<int32_t>& f_of_p) {
+  t_ptr.alloc(coarse_n + 1, c.s);
+  t_p.alloc(std::max<int64_t>(nnzf, 1), c.s);
+  f_of_p.alloc(std::max<int64_t>(nnzf, 1), c.s);
+  if (nnzf == 0) {
+    t_ptr.zero();
+    return;
+  }
+  DVec<uint32_t> key(nnzf, c.s);
+  DVec<int64_t> ids(nnzf, c.s);
+  stage_keys_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(nf, f_ptr, f_nbr, cop, key.p, f_of_p.p);
+  iota64_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(ids.p, nnzf);
+  CK_LAUNCH();
+  // stable sort of contribution indices p by target coarse node: within a
+  // target, p ascending == (f asc, p asc), the reference's accumulation order
+  int bits = 1;
+  while ((1ull << bits) <= (unsigned long long)coarse_n && bits < 32) ++bits;
+  DVec<uint64_t> k64(nnzf, c.s), k64s(nnzf, c.s);
+  widen_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(key.p, nnzf, k64.p);
+  CK_LAUNCH();
+  sort_pairs_u64(c, k64.p, k64s.p, ids.p, t_p.p, nnzf, bits);
+  seg_bounds64_kernel<<<blocks_for(nnzf + 1), kThreads, 0, c.s>>>(k64s.p, nnzf, coarse_n, t_ptr.p);
+  CK_LAUNCH();
+}
+
+__global__ void agg_keys_kernel(const int32_t* agg, int32_t n, uint64_t* key, int32_t* ids) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  key[u] = (uint64_t)(uint32_t)agg[u];
+  ids[u] = u;
+}
+void build_members(Ctx& c, int32_t fine_n, int32_t coarse_n, const int32_t* agg,
+                   DVec<int64_t>& mem_ptr, DVec<int32_t>& mem) {
+  mem_ptr.alloc(coarse_n + 1, c.s);
+  mem.alloc(fine_n, c.s);
+  DVec<uint64_t> key(fine_n, c.s), key_sorted(fine_n, c.s);
+  DVec<int32_t> ids(fine_n, c.s);
+  agg_keys_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(agg, fine_n, key.p, ids.p);
+  CK_LAUNCH();
+  int bits = 1;
+  while ((1ull << bits) <= (unsigned long long)coarse_n && bits < 32) ++bits;
+  sort_pairs_u64_i32(c, key.p, key_sorted.p, ids.p, mem.p, fine_n, bits);
+  seg_bounds64_kernel<<<blocks_for(fine_n + 1), kThreads, 0, c.s>>>(key_sorted.p, fine_n, coarse_n, mem_ptr.p);
+  CK_LAUNCH();
+}
+
+}  // namespace lamgb

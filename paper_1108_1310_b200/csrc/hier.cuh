@@ -1,0 +1,123 @@
+// hier.cuh -- device-resident hierarchy (lamg::Hierarchy, hierarchy.hpp:24-50).
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "core.cuh"
+
+namespace lamgb {
+
+enum LevelKind { KIND_FINEST = 0, KIND_ELIM = 1, KIND_AGG = 2, KIND_COARSEST = 3 };
+enum CoarsestMode { CM_NONE = 0, CM_DIRECT = 1, CM_RELAX = 2 };
+
+// lamg::ElimStage (elimination.hpp:16-26) + solve-time transpose lists
+struct DStage {
+  int32_t parent_n = 0, coarse_n = 0, nf = 0;
+  int64_t nnzf = 0;
+  DVec<int32_t> f_nodes;
+  DVec<double> f_diag;
+  DVec<int64_t> f_ptr;
+  DVec<int32_t> f_nbr;
+  DVec<double> f_val;
+  DVec<int32_t> cop, poc;
+  DVec<int64_t> t_ptr, t_p;
+  DVec<int32_t> f_of_p;
+  StageV view() const {
+    return StageV{parent_n, coarse_n, nf, f_nodes.p, f_diag.p, f_ptr.p, f_nbr.p, f_val.p,
+                  cop.p, poc.p, t_ptr.p, t_p.p, f_of_p.p};
+  }
+};
+
+// lamg::AggregationTransfer (aggregation.hpp:36-44) + member lists
+struct DAgg {
+  int32_t fine_n = 0, coarse_n = 0;
+  int stage_used = 1;
+  double alpha = 1.0;
+  int32_t dummy_aggregate = -1;
+  DVec<int32_t> aggregate_of, seed_of;
+  DVec<int64_t> mem_ptr;
+  DVec<int32_t> mem;
+};
+
+// Coarsest direct solver: bordered [[A,1],[1^T,0]] LU per connected component
+// (coarse_solver.cpp:14-45), factored on the device at setup.
+struct DDirect {
+  int32_t n = 0, ncomp = 0, maxN = 0;
+  int64_t m = 0;
+  std::vector<int32_t> comp_size;  // host copy
+  DVec<int32_t> comp_start;        // [ncomp+1] offsets into nodes
+  DVec<int32_t> nodes;             // nodes of each component, ascending
+  DVec<int64_t> lu_off;            // [ncomp] offsets into lu
+  DVec<double> lu;                 // (cn+1)^2 row-major per component
+  DVec<int32_t> perm;              // (cn+1) per component, offsets comp_start[c]+c
+  DVec<double> inv;                // throughput: first n columns of the inverse rows
+};
+
+struct DLevel {
+  int kind = KIND_FINEST;
+  DCSR op;
+  std::vector<std::unique_ptr<DStage>> stages;  // elimination transfer
+  std::unique_ptr<DAgg> agg;                    // aggregation transfer
+  double gamma = 1.0;
+  int nu_pre = 0, nu_post = 0, tv_count = 0;
+  int coarsest = CM_NONE;
+  std::unique_ptr<DDirect> direct;
+  Schedule sched;          // exact-order GS wavefronts of this level's operator
+  UpperIndex upper;        // energy / relaxation helpers
+};
+
+struct DHier {
+  std::vector<std::unique_ptr<DLevel>> levels;
+  double setup_work = 0.0;
+  double setup_seconds = 0.0;
+  uint64_t seed = 0;
+  std::vector<std::string> warnings;
+  int device = 0;
+  cudaStream_t owner_stream = nullptr;
+  // throughput mode (colour-permuted copies), built on demand
+  struct Throughput* tp = nullptr;
+  ~DHier();
+};
+
+struct SetupOpts {
+  double gamma = 1.5;
+  uint64_t seed = 1;
+  int32_t coarsest_n = 150;
+  int tv_sweeps = 3, tv_count_finest = 4, tv_count_max = 10;
+};
+
+// hierarchy.cpp:59-138
+std::unique_ptr<DHier> setup_device(Ctx& c, const CSRv& a, const SetupOpts& o);
+// hierarchy.cpp:31-40
+double level_cycle_index(const DHier& h, size_t l, double gamma);
+
+// ---- building blocks exposed for the per-kernel API -----------------------
+struct SelectResult {
+  int32_t nf = 0, nc = 0;
+  DVec<int32_t> f, c;
+};
+void select_low_degree(Ctx& c, const CSRv& a, int32_t max_degree, SelectResult& out);
+// schur_reduce: fills stage arrays and the coarse operator; throws like the reference
+void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int32_t* cset,
+                  int32_t nc, DStage& st, DCSR& coarse, bool check_inputs);
+// eliminate_rounds: false when the first round already selects too few nodes
+bool eliminate_rounds(Ctx& c, const CSRv& a, std::vector<std::unique_ptr<DStage>>& stages,
+                      DCSR& coarse);
+double probe_relaxation(Ctx& c, const CSRv& a, const Schedule& sch, const UpperIndex& up,
+                        int sweeps, uint64_t seed);
+void generate_tvs(Ctx& c, const CSRv& a, const Schedule& sch, int K, int sweeps, uint64_t seed,
+                  DVec<double>& X /* n*K node-major */);
+void compute_affinities(Ctx& c, const CSRv& a, int K, const double* X, double* aff, double* nn);
+int32_t detect_hubs(Ctx& c, const CSRv& a, DVec<int32_t>& hubs);
+void aggregate(Ctx& c, const CSRv& a, int K, const double* X, double gamma, const int32_t* hubs,
+               int32_t nhubs, DAgg& out, int* stages_run);
+void galerkin(Ctx& c, const CSRv& a, const int32_t* agg, int32_t coarse_n, DCSR& out);
+void make_direct(Ctx& c, const CSRv& a, DDirect& d);
+// scratch: 2*maxN + 2 doubles
+void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exact, double* scratch);
+void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, double* x,
+                 DVec<double>& r, int* sweeps_out, bool exact);
+
+}  // namespace lamgb

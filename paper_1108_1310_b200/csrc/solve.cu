@@ -1,0 +1,437 @@
+// solve.cu -- the solve phase: energy-corrected cycle (cycle.cpp:107-273).
+//
+// Control flow is host C++ mirroring CycleDriver: per-level credits decide
+// the fan-out, each level's work is a short sequence of device kernels on
+// the context stream. Vectors never leave the device; the host reads one
+// scalar per cycle (the residual norm that drives convergence/divergence).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "solve.cuh"
+
+namespace lamgb {
+
+uint64_t rng_derive_host(uint64_t seed, uint64_t stream);
+
+struct Throughput {};
+DHier::~DHier() { delete tp; }
+
+int LevelCredits::take(size_t l, double gamma) {
+  if (credit.size() <= l) credit.resize(l + 1, 0.0);
+  credit[l] += gamma;
+  int theta = std::max(1, (int)std::floor(credit[l]));
+  credit[l] -= theta;
+  if (credit[l] < 0.0) credit[l] = 0.0;
+  return theta;
+}
+
+// ---------------------------------------------------------------- profiling
+static void prof_mark(Ctx& c, int cls, bool begin, double bytes = 0.0) {
+  if (!c.prof.enabled) return;
+  auto& ev = c.prof.ev[cls];
+  int64_t idx = 2 * c.prof.used[cls] + (begin ? 0 : 1);
+  while ((int64_t)ev.size() <= idx) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ev.push_back(e);
+  }
+  CK(cudaEventRecord(ev[idx], c.s));
+  if (!begin) {
+    ++c.prof.used[cls];
+    c.prof.bytes[cls] = bytes;
+  }
+}
+
+// ------------------------------------------------------------- workspace
+void Workspace::ensure(Ctx& c, const DHier& h) {
+  if (owner == &h && lv.size() == h.levels.size()) return;
+  owner = &h;
+  lv.clear();
+  lv.resize(h.levels.size());
+  int32_t maxN = 0;
+  for (size_t l = 0; l < h.levels.size(); ++l) {
+    const DLevel& L = *h.levels[l];
+    LevelWS& w = lv[l];
+    const int32_t n = L.op.n;
+    if (l > 0) {
+      w.b.alloc(n, c.s);
+      w.x.alloc(n, c.s);
+    }
+    w.r.alloc(n, c.s);
+    if (L.direct) maxN = std::max(maxN, L.direct->maxN);
+    if (l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_ELIM) {
+      const auto& st = h.levels[l + 1]->stages;
+      w.stage_rhs.resize(st.size());
+      w.stage_x.resize(st.size());
+      for (size_t s = 1; s < st.size(); ++s) {
+        w.stage_rhs[s].alloc(st[s]->parent_n, c.s);
+        w.stage_x[s].alloc(st[s]->parent_n, c.s);
+      }
+    }
+  }
+  direct_scratch.alloc(2 * (int64_t)maxN + 2, c.s);
+  top_rhs_valid = false;
+}
+
+void Workspace::ensure_adaptive(Ctx& c, const DHier& h) {
+  for (size_t l = 0; l < h.levels.size(); ++l) {
+    LevelWS& w = lv[l];
+    const int32_t n = h.levels[l]->op.n;
+    if (w.saved_x[0].n >= n) continue;
+    for (int i = 0; i < 2; ++i) {
+      w.saved_x[i].alloc(n, c.s);
+      w.saved_r[i].alloc(n, c.s);
+    }
+    w.tmp.alloc(n, c.s);
+  }
+}
+
+// -------------------------------------------------------------- reductions
+static void fold_sum(Ctx& c, bool exact, const double* x, int64_t n, double* d_out) {
+  if (exact) seq_sum(c, x, n, d_out);
+  else tree_sum(c, x, n, d_out);
+}
+static void fold_norm2(Ctx& c, bool exact, const double* x, int64_t n, double* d_out) {
+  if (exact) seq_norm2(c, x, n, d_out);
+  else tree_norm2(c, x, n, d_out);
+}
+static void sub_mean(Ctx& c, bool exact, double* x, int64_t n) {
+  if (exact) subtract_mean_seq(c, x, n);
+  else subtract_mean_tree(c, x, n);
+}
+
+// ------------------------------------------------------------ recombination
+__global__ void diff_kernel(const double* a, const double* b, double* out, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] - b[i];
+}
+__global__ void prod_kernel(const double* a, const double* b, double* out, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] * b[i];
+}
+// dots[0]=r.r, [1+i]=c_i, [3..6]=g00,g01,g11 -> alpha[0..1] (cycle.cpp:216-257)
+__global__ void recomb_alpha_kernel(const double* dots, int cols, double* alpha) {
+  double r_norm2 = dots[0];
+  double c[2] = {dots[1], dots[2]};
+  double g[2][2] = {{dots[3], dots[4]}, {dots[4], dots[5]}};
+  double al[2] = {0.0, 0.0};
+  if (cols == 1) {
+    if (g[0][0] > 0.0) al[0] = c[0] / g[0][0];
+  } else if (cols == 2) {
+    double det = g[0][0] * g[1][1] - g[0][1] * g[0][1];
+    double gg = g[0][0] * g[1][1];
+    if (det > 1e-14 * (gg < 1e-300 ? 1e-300 : gg)) {
+      al[0] = (c[0] * g[1][1] - c[1] * g[0][1]) / det;
+      al[1] = (c[1] * g[0][0] - c[0] * g[0][1]) / det;
+    } else {
+      double gain0 = g[0][0] > 0.0 ? c[0] * c[0] / g[0][0] : 0.0;
+      double gain1 = g[1][1] > 0.0 ? c[1] * c[1] / g[1][1] : 0.0;
+      if (gain0 >= gain1 && g[0][0] > 0.0) al[0] = c[0] / g[0][0];
+      else if (g[1][1] > 0.0) al[1] = c[1] / g[1][1];
+    }
+  }
+  for (int i = 0; i < cols; ++i) al[i] = al[i] < -2.0 ? -2.0 : (2.0 < al[i] ? 2.0 : al[i]);
+  double predicted = r_norm2;
+  for (int i = 0; i < cols; ++i) {
+    predicted -= 2.0 * al[i] * c[i];
+    for (int j = 0; j < cols; ++j) predicted += al[i] * g[i][j] * al[j];
+  }
+  if (predicted > r_norm2) al[0] = al[1] = 0.0;
+  alpha[0] = al[0];
+  alpha[1] = al[1];
+}
+// rk = r - sum alpha_i ad_i (ad_i = r - saved_r_i); x += sum alpha_i (saved_x_i - x)
+__global__ void recomb_update_kernel(int64_t n, int cols, const double* alpha, const double* r,
+                                     const double* sr0, const double* sr1, const double* sx0,
+                                     const double* sx1, double* x, double* rk2) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double rk = r[k], xk = x[k], delta = 0.0;
+  const double* sr[2] = {sr0, sr1};
+  const double* sx[2] = {sx0, sx1};
+  for (int i = 0; i < cols; ++i) {
+    double ad = r[k] - sr[i][k];
+    rk -= alpha[i] * ad;
+    delta += alpha[i] * (sx[i][k] - xk);
+  }
+  rk2[k] = rk * rk;
+  x[k] = xk + delta;
+}
+__global__ void recomb_finish_kernel(const double* dots, const double* new2, double* growth) {
+  double before = sqrt(dots[0]);
+  double nn = *new2;
+  double after = sqrt(nn < 0.0 ? 0.0 : nn);
+  if (before > 0.0) {
+    double g = after / before;
+    if (*growth < g) *growth = g;
+  }
+}
+
+// recombine (cycle.cpp:23-103) with the reference's fold order in every dot
+static void recombine(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS& w, double* x,
+                      bool exact, double* growth) {
+  const int64_t n = a.n;
+  residual_exact(c, a, b, x, w.r.p);
+  c.work += (double)a.m;
+  double* dots = c.dscal + 120;  // [120..126]
+  CK(cudaMemsetAsync(dots, 0, 7 * sizeof(double), c.s));
+  prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.r.p, w.tmp.p, n);
+  fold_sum(c, exact, w.tmp.p, n, dots + 0);
+  DVec<double> ad[2];
+  for (int i = 0; i < cols; ++i) {
+    ad[i].alloc(n, c.s);
+    diff_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.saved_r[i].p, ad[i].p, n);
+  }
+  for (int i = 0; i < cols; ++i) {
+    prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, ad[i].p, w.tmp.p, n);
+    fold_sum(c, exact, w.tmp.p, n, dots + 1 + i);
+    for (int j = 0; j <= i; ++j) {
+      prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ad[i].p, ad[j].p, w.tmp.p, n);
+      int slot = (i == 0 && j == 0) ? 3 : (i == 1 && j == 0) ? 4 : 5;
+      fold_sum(c, exact, w.tmp.p, n, dots + slot);
+    }
+  }
+  double* alpha = c.dscal + 130;
+  recomb_alpha_kernel<<<1, 1, 0, c.s>>>(dots, cols, alpha);
+  recomb_update_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, cols, alpha, w.r.p, w.saved_r[0].p,
+                                                            cols > 1 ? w.saved_r[1].p : w.saved_r[0].p,
+                                                            w.saved_x[0].p, cols > 1 ? w.saved_x[1].p : w.saved_x[0].p,
+                                                            x, w.tmp.p);
+  fold_sum(c, exact, w.tmp.p, n, dots + 6);
+  recomb_finish_kernel<<<1, 1, 0, c.s>>>(dots, dots + 6, growth);
+  CK_LAUNCH();
+  c.work += (double)cols * (double)n;
+}
+
+void recombine_api(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS& w, double* x, bool exact,
+                   double* growth) {
+  recombine(c, a, b, cols, w, x, exact, growth);
+}
+
+// ------------------------------------------------------------------ driver
+struct Driver {
+  Ctx& c;
+  const DHier& h;
+  const CycleCfg& cfg;
+  Workspace& ws;
+  LevelCredits credits;
+  bool exact;
+  double* growth;
+  int64_t recombinations = 0;
+  int relax_sweeps = 0;
+
+  void visit(size_t l, const double* b, double* x, int theta) {
+    const DLevel& L = *h.levels[l];
+    if (L.coarsest != CM_NONE) {
+      coarsest(l, b, x);
+      return;
+    }
+    if (h.levels[l + 1]->kind == KIND_ELIM) visit_elimination(l, b, x, theta);
+    else visit_aggregation(l, b, x, theta);
+  }
+
+  void coarsest(size_t l, const double* b, double* x) {
+    const DLevel& L = *h.levels[l];
+    if (L.coarsest == CM_DIRECT) {
+      direct_solve(c, *L.direct, b, x, exact, ws.direct_scratch.p);
+    } else {
+      int sw = 0;
+      relax_solve(c, L.op.view(), L.sched, b, x, ws.lv[l].r, &sw, exact);
+      relax_sweeps += sw;
+    }
+  }
+
+  // cycle.cpp:131-164
+  void visit_elimination(size_t l, const double* b, double* x, int theta) {
+    const DLevel& child = *h.levels[l + 1];
+    const auto& st = child.stages;
+    const size_t S = st.size();
+    LevelWS& w = ws.lv[l];
+    LevelWS& wc = ws.lv[l + 1];
+    // stage_rhs[0] = b; stage_rhs[s] = coarsened; coarse rhs -> child's b
+    std::vector<const double*> rhs(S);
+    rhs[0] = b;
+    const bool cached = l == 0 && ws.top_rhs_valid;
+    for (size_t s = 0; s < S; ++s) {
+      double* out = s + 1 < S ? w.stage_rhs[s + 1].p : wc.b.p;
+      if (!cached) {
+        coarsen_rhs(c, st[s]->view(), rhs[s], out);
+        c.work += (double)st[s]->nnzf;
+      }
+      if (s + 1 < S) rhs[s + 1] = out;
+    }
+    if (l == 0) ws.top_rhs_valid = true;
+    for (int i = 0; i < theta; ++i) {
+      const double* cur = x;
+      for (size_t s = 0; s < S; ++s) {
+        double* out = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
+        inject(c, st[s]->view(), cur, out);
+        cur = out;
+      }
+      int theta_child = credits.take(l + 1, child.gamma);
+      visit(l + 1, wc.b.p, wc.x.p, theta_child);
+      for (size_t s = S; s-- > 0;) {
+        const double* xc = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
+        double* out = s == 0 ? x : w.stage_x[s].p;
+        backsub(c, st[s]->view(), xc, rhs[s], out);
+        c.work += (double)st[s]->nnzf;
+      }
+    }
+  }
+
+  void gs(size_t l, const double* b, double* x, int sweeps) {
+    const DLevel& L = *h.levels[l];
+    const bool p = l == 0;
+    if (p) prof_mark(c, 0, true);
+    gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
+    if (p) prof_mark(c, 0, false, (24.0 * L.op.m + 40.0 * L.op.n + 8.0) * sweeps);
+    c.work += (double)L.op.m * sweeps;
+  }
+  void resid(size_t l, const double* b, const double* x, double* r) {
+    const DLevel& L = *h.levels[l];
+    const bool p = l == 0;
+    if (p) prof_mark(c, 1, true);
+    residual_exact(c, L.op.view(), b, x, r);
+    if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 40.0 * L.op.n + 8.0);
+    c.work += (double)L.op.m;
+  }
+
+  // cycle.cpp:176-209
+  void visit_aggregation(size_t l, const double* b, double* x, int theta) {
+    const DLevel& L = *h.levels[l];
+    const DLevel& child = *h.levels[l + 1];
+    const DAgg& t = *child.agg;
+    LevelWS& w = ws.lv[l];
+    LevelWS& wc = ws.lv[l + 1];
+    const bool adaptive = cfg.correction == 1;
+    int nsaved = 0;
+    for (int i = 0; i < theta; ++i) {
+      if (child.nu_pre) gs(l, b, x, child.nu_pre);
+      resid(l, b, x, w.r.p);
+      if (adaptive) {
+        if (nsaved >= 2) throw LamgError(LAMG_E_ERROR, "recombination supports at most two saved iterates");
+        copy_d(c, w.saved_x[nsaved].p, x, L.op.n);
+        copy_d(c, w.saved_r[nsaved].p, w.r.p, L.op.n);
+        ++nsaved;
+      }
+      restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p);
+      wc.x.zero();
+      int theta_child = credits.take(l + 1, child.gamma);
+      visit(l + 1, wc.b.p, wc.x.p, theta_child);
+      interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
+      if (child.nu_post) gs(l, b, x, child.nu_post);
+    }
+    if (adaptive && nsaved > 0) {
+      recombine(c, L.op.view(), b, nsaved, w, x, exact, growth);
+      ++recombinations;
+    }
+  }
+};
+
+// ------------------------------------------------------------ solve entry
+__global__ void absmax_kernel(const double* x, int64_t n, unsigned long long* out) {
+  __shared__ double sh[kThreads];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(sh[0]));
+}
+
+static std::string to_string_f(double v) {
+  char buf[64];
+  snprintf(buf, sizeof buf, "%f", v);
+  return buf;
+}
+
+// cycle.cpp:221-273; b, x0, x are device pointers of the finest size
+int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
+                 double* x, SolveResult& res) {
+  const DLevel& L0 = *h.levels[0];
+  const CSRv a = L0.op.view();
+  const int64_t n = a.n;
+  const bool exact = c.mode == LAMG_MODE_VALIDATE;
+  res = SolveResult{};
+  // compatibility: |sum b| <= 1e-10 ||b||_inf (sequential fold, exact max)
+  unsigned long long* bmax = (unsigned long long*)(c.dscal + 140);
+  double* bsum = c.dscal + 141;
+  CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), c.s));
+  absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
+  CK_LAUNCH();
+  seq_sum(c, b, n, bsum);
+  CK(cudaMemcpyAsync(c.hscal, c.dscal + 140, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  double b_inf, b_sum = c.hscal[1];
+  {
+    unsigned long long bits;
+    memcpy(&bits, &c.hscal[0], sizeof bits);
+    memcpy(&b_inf, &bits, sizeof b_inf);
+  }
+  if (std::fabs(b_sum) > 1e-10 * b_inf)
+    throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
+
+  if (!c.ws) c.ws = new Workspace();
+  Workspace& ws = *c.ws;
+  ws.ensure(c, h);
+  ws.top_rhs_valid = false;
+  if (cfg.correction == 1) ws.ensure_adaptive(c, h);
+  const double w0 = c.work = 0.0;
+  copy_d(c, x, x0, n);
+  double* rn_d = c.dscal + 150;
+  double* growth = c.dscal + 151;
+  CK(cudaMemsetAsync(growth, 0, sizeof(double), c.s));
+  Driver d{c, h, cfg, ws, LevelCredits{}, exact, growth};
+  d.credits.credit.assign(h.levels.size(), 0.0);
+  d.resid(0, b, x, ws.lv[0].r.p);
+  fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
+  const double r0 = read_scalar(c, rn_d);
+  res.residuals.push_back(r0);
+  if (r0 == 0.0) {
+    sub_mean(c, exact, x, n);
+    c.sync();
+    res.converged = true;
+    res.acf = 0.0;
+    res.solve_work = (c.work - w0) / (double)a.m;
+    return LAMG_OK;
+  }
+  const double target = r0 / cfg.target_reduction;
+  int rc = LAMG_OK;
+  for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
+    d.visit(0, b, x, 1);
+    sub_mean(c, exact, x, n);
+    d.resid(0, b, x, ws.lv[0].r.p);
+    fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
+    const double rn = read_scalar(c, rn_d);
+    res.residuals.push_back(rn);
+    res.cycles = cycle;
+    if (rn <= target) {
+      res.converged = true;
+      break;
+    }
+    if (rn > cfg.divergence_factor * r0 || !std::isfinite(rn)) {
+      res.acf = std::pow(rn / r0, 1.0 / cycle);
+      res.solve_work = (c.work - w0) / (double)a.m;
+      res.message = "solve diverged: residual grew from " + to_string_f(r0) + " to " + to_string_f(rn);
+      rc = LAMG_E_DIVERGED;
+      break;
+    }
+  }
+  if (rc == LAMG_OK) {
+    const double rp = res.residuals.back();
+    res.acf = std::pow(rp / r0, 1.0 / (double)res.cycles);
+    res.solve_work = (c.work - w0) / (double)a.m;
+  }
+  res.recombinations = d.recombinations;
+  res.recomb_max_growth = read_scalar(c, growth);
+  res.relax_sweeps = d.relax_sweeps;
+  return rc;
+}
+
+}  // namespace lamgb

@@ -1,0 +1,62 @@
+// solve.cuh -- solve-phase driver declarations.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "hier.cuh"
+
+namespace lamgb {
+
+// lamg::CycleConfig (cycle.hpp:28-36)
+struct CycleCfg {
+  int correction = 0;  // 0 Flat, 1 AdaptiveRecombination
+  double mu = 4.0 / 3.0;
+  int max_cycles = 300;
+  double target_reduction = 1e10;
+  double divergence_factor = 1e3;
+};
+
+// lamg::SolveStats (cycle.hpp:38-46)
+struct SolveResult {
+  std::vector<double> residuals;
+  double acf = 0.0;
+  double solve_work = 0.0;
+  int cycles = 0;
+  bool converged = false;
+  int64_t recombinations = 0;
+  double recomb_max_growth = 0.0;
+  int relax_sweeps = 0;
+  std::string message;
+};
+
+// LevelCredit (cycle.cpp:14-21)
+struct LevelCredits {
+  std::vector<double> credit;
+  int take(size_t l, double gamma);
+};
+
+struct LevelWS {
+  DVec<double> b, x, r;
+  std::vector<DVec<double>> stage_rhs, stage_x;  // index s >= 1
+  DVec<double> saved_x[2], saved_r[2], tmp;
+};
+
+// per-context solve workspace, sized for the last hierarchy solved
+struct Workspace {
+  const DHier* owner = nullptr;
+  std::vector<LevelWS> lv;
+  DVec<double> direct_scratch;
+  bool top_rhs_valid = false;
+  void ensure(Ctx& c, const DHier& h);
+  void ensure_adaptive(Ctx& c, const DHier& h);
+};
+
+// recombine (cycle.cpp:23-103); dots land in c.dscal[120..126]
+void recombine_api(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS& w, double* x, bool exact,
+                   double* growth);
+
+int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
+                 double* x, SolveResult& res);
+
+}  // namespace lamgb
