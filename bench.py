@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 LAMG hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lamg|reference]
+                    [--mode throughput|validate] [--config 2]
+
+A step is one full LAMG solve (to the reference's relative residual 1e-10)
+of BASELINE.json config 2 -- the 3D 7-point 128^3 Laplacian with seeded
+log-uniform weights -- over a hierarchy built once on the GPU (setup is
+timed separately and reported). `value` is fine-level edges*cycles/s of the
+whole job (sum over ranks of m1 * cycles per step / max-over-ranks device
+time), inputs resident in HBM; `e2e` is the same metric through the public
+C-ABI call with host buffers (H2D of b and x0, D2H of x and the residual
+history inside the timed region). Multi-GPU runs are independent replicas,
+each solving its own right-hand side (RHS sharding: weak scaling).
+
+`--impl reference` times the reference's own CPU solve (oracle/_ref, the
+unmodified reference core) on the host cores with one solve per thread.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_PEAK_FALLBACK = 6650.0
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ dist
+class Dist:
+    def __init__(self, want_gpu: bool):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if (want_gpu and torch.cuda.is_available()) else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.backend = dist, backend
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def allreduce(self, v: float, op: str) -> float:
+        if self.world == 1:
+            return v
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(self.rows), "reasons": reasons}
+
+
+# ------------------------------------------------------------------ inputs
+WORKLOADS = {
+    1: "cfg1: 2D 5-point grid 256^2 (n=65,536), unit weights, Gaussian zero-sum b, to 1e-10",
+    2: "cfg2: 3D 7-point grid 128^3 (n=2,097,152, m=6,242,304), weights 10^U[-3,3], Gaussian zero-sum b, to 1e-10",
+}
+
+
+def build_inputs(cfg: int, rank: int):
+    from paper_1108_1310_b200 import graphs as G
+    a = G.make_config(cfg)
+    b = G.gaussian_rhs(a.n, 100 + cfg + 1000 * rank)
+    x0 = G.default_x0(a.n, seed=1 + rank)
+    return a, b, x0
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+# ------------------------------------------------------------------- lamg
+def run_lamg(args, dist: Dist):
+    import torch
+    from paper_1108_1310_b200 import _lib
+    from paper_1108_1310_b200 import lamg as L
+
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    a, b, x0 = build_inputs(args.config, dist.rank)
+    log(f"[rank {dist.rank}] inputs n={a.n} m={a.m} built in {time.time() - t0:.1f}s")
+    mode = L.MODE_THROUGHPUT if args.mode == "throughput" else L.MODE_VALIDATE
+    ctx = L.Context(dev, mode)
+    lib = ctx.lib
+    lib.lamg_ctx_stream.restype = C.c_void_p
+    sptr = lib.lamg_ctx_stream(ctx.p)
+    stream = torch.cuda.ExternalStream(sptr, device=dev)
+
+    # setup (device), timed on its own
+    torch.cuda.synchronize()
+    ts = time.time()
+    h = L.setup(a, ctx=ctx)
+    torch.cuda.synchronize()
+    setup_s = time.time() - ts
+    if mode == L.MODE_THROUGHPUT:
+        L._check(lib.lamg_hier_prepare_throughput(ctx.p, h.h))
+    log(f"[rank {dist.rank}] setup {setup_s:.2f}s, {h.nlevels} levels")
+
+    n = a.n
+    db = torch.from_numpy(b).to(f"cuda:{dev}")
+    dx0 = torch.from_numpy(x0).to(f"cuda:{dev}")
+    dx = torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}")
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    cfg = L.CycleConfig().c()
+    st = L._lib.lamg_solve_stats()
+    res = np.empty(512)
+    torch.cuda.synchronize()
+
+    def solve_dev():
+        code = lib.lamg_solve_dev(ctx.p, h.h, C.c_void_p(db.data_ptr()), C.c_void_p(dx0.data_ptr()), C.byref(cfg),
+                                  C.c_void_p(dx.data_ptr()), C.byref(st), res.ctypes.data_as(C.c_void_p),
+                                  C.c_int32(512))
+        L._check(code)
+        return st.cycles
+
+    def flush_l2():
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+
+    for _ in range(args.warmup):
+        solve_dev()
+    # timed region: K solves, L2 flushed between steps (outside the events)
+    lib.lamg_ctx_profile(ctx.p, 1)
+    clocks = ClockSampler(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = lib.lamg_launch_count()
+    evs = []
+    cycles = []
+    for _ in range(args.steps):
+        flush_l2()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        cycles.append(solve_dev())
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = lib.lamg_launch_count() - launches0
+    dist.barrier()
+    clk = clocks.stop()
+    lib.lamg_ctx_profile(ctx.p, 0)
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    local_ms = sum(step_ms)
+    units = float(sum(cycles)) * a.m
+    max_ms = dist.allreduce(local_ms, "MAX")
+    tot_units = dist.allreduce(units, "SUM")
+    value = tot_units / (max_ms / 1e3)
+
+    # kernel roofline from the events recorded around the finest-level launches
+    hbm, hbm_src = peaks()
+    kern = {}
+    for k, name in ((0, "gs_finest"), (1, "residual_finest")):
+        nl, tm, by = C.c_int64(), C.c_double(), C.c_double()
+        lib.lamg_ctx_profile_read(ctx.p, C.c_int(k), C.byref(nl), C.byref(tm), C.byref(by))
+        if nl.value:
+            avg_ms = tm.value / nl.value
+            kern[name] = {"launches": nl.value, "avg_ms": avg_ms, "bytes": by.value,
+                          "gbs": by.value / (avg_ms / 1e3) / 1e9, "share": tm.value / local_ms}
+    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if dom and os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.mode}:{dom}")
+    roof = None
+    if dom:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(kern[dom]["gbs"], 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(kern[dom]["gbs"] / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
+                "algorithmic_bytes_per_launch": kern[dom]["bytes"], "avg_launch_ms": round(kern[dom]["avg_ms"], 5),
+                "share_of_step": round(kern[dom]["share"], 3),
+                "kernels": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                            for k, v in kern.items()}}
+
+    # end to end through the public C-ABI with host buffers
+    hb = torch.from_numpy(b).pin_memory().numpy()
+    hx0 = torch.from_numpy(x0).pin_memory().numpy()
+    hx = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    e2e_ms, e2e_units = 0.0, 0.0
+    for i in range(args.warmup + args.steps):
+        flush_l2()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        xo, so = L.solve(h, hb, hx0, L.CycleConfig(), ctx=ctx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms += e0.elapsed_time(e1)
+            e2e_units += so.cycles * a.m
+    e2e_max = dist.allreduce(e2e_ms, "MAX")
+    e2e_units = dist.allreduce(e2e_units, "SUM")
+    e2e_value = e2e_units / (e2e_max / 1e3)
+
+    # validation-mode solve of the same system (bit-exact path) for the report
+    extra = {}
+    if dist.rank == 0 and not args.skip_validate:
+        ctx.set_mode(L.MODE_VALIDATE)
+        tv = time.time()
+        xv, sv = L.solve(h, b, x0, L.CycleConfig(), ctx=ctx)
+        extra["validate_mode"] = {"cycles": sv.cycles, "solve_s": round(time.time() - tv, 3), "x_sha": sha(xv)}
+        gl = os.path.join(ROOT, "tests", "golden", "large.json")
+        key = {1: "cfg1_grid5_256", 2: "cfg2_grid3d_128"}.get(args.config)
+        if os.path.exists(gl) and key in json.load(open(gl)):
+            g = json.load(open(gl))[key]
+            if g["b_sha"] == sha(b) and g["x0_sha"] == sha(x0):
+                extra["validate_mode"]["reference_cycles"] = g["cycles"]
+                extra["validate_mode"]["x_bit_identical_to_reference"] = g["x_sha"] == sha(xv)
+        xt = xo
+        extra["throughput_vs_validate_rel_x_diff"] = float(np.linalg.norm(xt - xv) / np.linalg.norm(xv))
+        ctx.set_mode(mode)
+
+    out = None
+    if dist.rank == 0:
+        cpu = None if args.no_cpu_baseline or dist.world > 1 else cpu_baseline(a, b, x0, args)
+        out = {
+            "metric": "fine-level edges*cycles/s (solve to relative residual 1e-10)",
+            "value": value, "unit": "edges*cycles/s", "n_gpus": dist.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded generator for BASELINE.json config %d (no dataset involved)" % args.config,
+            "config": {"workload": WORKLOADS[args.config], "n": a.n, "m": a.m, "mode": args.mode,
+                       "levels": h.nlevels, "cycles_per_solve": cycles[0], "setup_s": round(setup_s, 3),
+                       "solve_ms": round(local_ms / args.steps, 3),
+                       "l2": "L2 flushed (256 MB write) between timed steps; finest operator 183 MB > 126 MB L2",
+                       "parallelism": f"replicas x{dist.world} (one RHS per GPU, no data-path collective)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "edges*cycles/s", "h2d_bytes_per_step": 16 * n,
+                    "d2h_bytes_per_step": 8 * n + 8 * (cycles[0] + 1)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        out.update(extra)
+    ctx.close()
+    return out
+
+
+# -------------------------------------------------------------- CPU arms
+def _ref_oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import LIBS, Oracle
+    if os.path.exists(LIBS["ref"][0]):
+        return Oracle("ref"), "reference"
+    return Oracle("port"), "port"
+
+
+def cpu_baseline(a, b, x0, args):
+    """Reference CPU solve on a bounded sample: 1 RHS, a few cycles, 1 core,
+    after a full (untimed) reference setup of the same operator."""
+    o, kind = _ref_oracle()
+    t = time.time()
+    h = o.setup(a)
+    setup_s = time.time() - t
+    cyc = args.cpu_cycles
+    secs, c = h.solve_batch(b[None, :], x0[None, :], 1, max_cycles=cyc)
+    v = a.m * float(c[0]) / secs
+    return {"value": v, "unit": "edges*cycles/s", "cores": 1, "kind": kind,
+            "sample": f"{int(c[0])} cycles of one reference solve (max_cycles={cyc}) on the same operator, b and x0; "
+                      f"reference setup {setup_s:.1f}s untimed", "setup_s": round(setup_s, 2)}
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return None
+    a, b, x0 = build_inputs(args.config, 0)
+    o, kind = _ref_oracle()
+    t = time.time()
+    h = o.setup(a)
+    setup_s = time.time() - t
+    threads = os.cpu_count() or 1
+    from paper_1108_1310_b200 import graphs as G
+    B = np.stack([G.gaussian_rhs(a.n, 100 + args.config + 1000 * i) for i in range(threads)])
+    X0 = np.stack([G.default_x0(a.n, seed=1 + i) for i in range(threads)])
+    cyc = args.cpu_cycles
+    for _ in range(args.warmup):
+        h.solve_batch(B[:1], X0[:1], 1, max_cycles=1)
+    tot, units = 0.0, 0.0
+    for _ in range(args.steps):
+        secs, c = h.solve_batch(B, X0, threads, max_cycles=cyc)
+        tot += secs
+        units += float(c.sum()) * a.m
+    v = units / tot
+    return {"metric": "fine-level edges*cycles/s (solve to relative residual 1e-10)", "value": v,
+            "unit": "edges*cycles/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic: seeded generator for BASELINE.json config %d" % args.config,
+            "config": {"workload": WORKLOADS[args.config], "n": a.n, "m": a.m, "reference_setup_s": round(setup_s, 2),
+                       "parallelism": f"{threads} host threads, one reference solve each"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "edges*cycles/s", "cores": threads, "kind": kind,
+                             "sample": f"per step {threads} concurrent reference solves x {cyc} cycles over one "
+                                       f"const hierarchy (solve is reentrant, SPEC.md:500)"},
+            "e2e": {"value": v, "unit": "edges*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["lamg", "reference"], default="lamg")
+    ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-cycles", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-validate", action="store_true")
+    args = ap.parse_args()
+    dist = Dist(want_gpu=args.impl == "lamg")
+    out = run_reference(args, dist) if args.impl == "reference" else run_lamg(args, dist)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

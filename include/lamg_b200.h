@@ -125,6 +125,10 @@ int lamg_ctx_set_mode(lamg_ctx *ctx, int mode);
 void lamg_ctx_destroy(lamg_ctx *ctx);
 const char *lamg_last_error(void);
 const char *lamg_version(void);
+/* kernels this library has launched so far (all contexts, monotone) */
+int64_t lamg_launch_count(void);
+/* the context's cudaStream_t, for callers that time or order work with it */
+void *lamg_ctx_stream(lamg_ctx *ctx);
 
 /* ---- setup: replaces lamg::setup (hierarchy.hpp:65; hierarchy.cpp:59-138) */
 int lamg_setup(lamg_ctx *ctx, const lamg_csr *a, int on_device, const lamg_setup_opts *opts,

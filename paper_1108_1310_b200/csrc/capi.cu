@@ -147,6 +147,10 @@ extern "C" {
 const char* lamg_last_error(void) { return g_err.c_str(); }
 const char* lamg_version(void) { return "lamg_b200 0.1 (sm_100a)"; }
 
+int64_t lamg_launch_count(void) { return (int64_t)g_launches.load(); }
+
+void* lamg_ctx_stream(lamg_ctx* ctx) { return ctx ? (void*)ctx->c.s : nullptr; }
+
 int lamg_ctx_create(int device, int mode, lamg_ctx** out) {
   *out = nullptr;
   return guarded([&] {

@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -21,6 +22,9 @@
 namespace lamgb {
 
 namespace cg = cooperative_groups;
+
+// kernels launched by this library (all contexts); lamg_launch_count()
+extern std::atomic<long long> g_launches;
 
 // ----------------------------------------------------------------- errors
 struct LamgError : std::runtime_error {

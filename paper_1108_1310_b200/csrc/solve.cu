@@ -177,30 +177,30 @@ static void recombine(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS&
   c.work += (double)a.m;
   double* dots = c.dscal + 120;  // [120..126]
   CK(cudaMemsetAsync(dots, 0, 7 * sizeof(double), c.s));
-  prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.r.p, w.tmp.p, n);
+  ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.r.p, w.tmp.p, n);
   fold_sum(c, exact, w.tmp.p, n, dots + 0);
   DVec<double> ad[2];
   for (int i = 0; i < cols; ++i) {
     ad[i].alloc(n, c.s);
-    diff_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.saved_r[i].p, ad[i].p, n);
+    ++g_launches, diff_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.saved_r[i].p, ad[i].p, n);
   }
   for (int i = 0; i < cols; ++i) {
-    prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, ad[i].p, w.tmp.p, n);
+    ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, ad[i].p, w.tmp.p, n);
     fold_sum(c, exact, w.tmp.p, n, dots + 1 + i);
     for (int j = 0; j <= i; ++j) {
-      prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ad[i].p, ad[j].p, w.tmp.p, n);
+      ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ad[i].p, ad[j].p, w.tmp.p, n);
       int slot = (i == 0 && j == 0) ? 3 : (i == 1 && j == 0) ? 4 : 5;
       fold_sum(c, exact, w.tmp.p, n, dots + slot);
     }
   }
   double* alpha = c.dscal + 130;
-  recomb_alpha_kernel<<<1, 1, 0, c.s>>>(dots, cols, alpha);
-  recomb_update_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, cols, alpha, w.r.p, w.saved_r[0].p,
+  ++g_launches, recomb_alpha_kernel<<<1, 1, 0, c.s>>>(dots, cols, alpha);
+  ++g_launches, recomb_update_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, cols, alpha, w.r.p, w.saved_r[0].p,
                                                             cols > 1 ? w.saved_r[1].p : w.saved_r[0].p,
                                                             w.saved_x[0].p, cols > 1 ? w.saved_x[1].p : w.saved_x[0].p,
                                                             x, w.tmp.p);
   fold_sum(c, exact, w.tmp.p, n, dots + 6);
-  recomb_finish_kernel<<<1, 1, 0, c.s>>>(dots, dots + 6, growth);
+  ++g_launches, recomb_finish_kernel<<<1, 1, 0, c.s>>>(dots, dots + 6, growth);
   CK_LAUNCH();
   c.work += (double)cols * (double)n;
 }
@@ -363,7 +363,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   unsigned long long* bmax = (unsigned long long*)(c.dscal + 140);
   double* bsum = c.dscal + 141;
   CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), c.s));
-  absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
+  ++g_launches, absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
   CK_LAUNCH();
   seq_sum(c, b, n, bsum);
   CK(cudaMemcpyAsync(c.hscal, c.dscal + 140, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
