@@ -294,6 +294,7 @@ int lamg_hier_level_info(const lamg_hier* h, int32_t l, lamg_level_info* o) {
       o->dummy_aggregate = L.agg->dummy_aggregate;
     }
     o->gs_fronts = L.sched.nfronts;
+    o->colors = L.color ? L.color->ncolors : 0;
   });
 }
 
@@ -376,8 +377,12 @@ int lamg_solve_dev(lamg_ctx* ctx, const lamg_hier* h, const double* b, const dou
 
 int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {
   return guarded([&] {
-    (void)ctx;
-    (void)h;
+    if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    set_device(ctx->c);
+    if (!h->h->throughput_ready) {
+      prepare_throughput(ctx->c, *h->h);
+      h->h->throughput_ready = true;
+    }
   });
 }
 
@@ -723,7 +728,7 @@ int lamg_k_coarsest_relax(lamg_ctx* ctx, const lamg_csr* a, const double* b, dou
     auto dx = up(c, x, a->n);
     DVec<double> r;
     int sw = 0;
-    relax_solve(c, av, sch, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
+    relax_solve(c, av, sch, nullptr, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
     dx.download(x, a->n);
     c.sync();
   });

@@ -214,33 +214,32 @@ int32_t read_i32(Ctx& c, const int32_t* d) {
 }
 
 // ------------------------------------------------------- bit-exact folds
-// A left-to-right fold is one dependent chain of fp64 adds; one warp stages
-// the operands (coalesced 32-wide loads, 8 tiles in flight) and lane 0 runs
-// the chain from registers broadcast through shuffles.
+// A left-to-right fold is one dependent chain of fp64 adds. One thread runs
+// it; loads are issued 32 at a time ahead of the chain (double-buffered) so
+// the chain, not memory latency, sets the pace.
 template <bool SQUARE>
 __global__ void seq_fold_kernel(const double* __restrict__ x, int64_t n, double* out) {
-  const int lane = threadIdx.x;
+  if (threadIdx.x != 0) return;
+  constexpr int B = 32;
   double s = 0.0;
-  constexpr int kTile = 32 * 8;
-  for (int64_t base = 0; base < n; base += kTile) {
-    double v[8];
+  double cur[B], nxt[B];
+  int64_t base = 0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      int64_t i = base + t * 32 + lane;
-      v[t] = i < n ? x[i] : 0.0;
+  for (int j = 0; j < B; ++j) cur[j] = j < n ? x[j] : 0.0;
+  for (; base < n; base += B) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) nxt[j] = base + B + j < n ? x[base + B + j] : 0.0;
+    const int cnt = n - base >= B ? B : (int)(n - base);
+    if (cnt == B) {
+#pragma unroll
+      for (int j = 0; j < B; ++j) s = s + (SQUARE ? cur[j] * cur[j] : cur[j]);
+    } else {
+      for (int j = 0; j < cnt; ++j) s = s + (SQUARE ? cur[j] * cur[j] : cur[j]);
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      int64_t rem = n - (base + t * 32);
-      int cnt = rem >= 32 ? 32 : (rem > 0 ? (int)rem : 0);
-      for (int j = 0; j < cnt; ++j) {
-        double y = __shfl_sync(0xffffffffu, v[t], j);
-        if (SQUARE) y = y * y;
-        s = s + y;
-      }
-    }
+    for (int j = 0; j < B; ++j) cur[j] = nxt[j];
   }
-  if (lane == 0) *out = SQUARE ? sqrt(s) : s;
+  *out = SQUARE ? sqrt(s) : s;
 }
 
 void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out) {

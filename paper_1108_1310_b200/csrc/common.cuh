@@ -234,6 +234,65 @@ __device__ inline void grid_barrier() {
   }
 }
 
+// Row fold s (-|+)= val[k] * x[col[k]] for k in [b, e), in k order (bit-exact
+// with the reference's sequential loop). Loads are issued in predicated
+// batches of U so a row costs ~2 memory latencies per batch instead of 2 per
+// nonzero: small colour phases and coarse levels are latency-bound.
+template <int U, bool SUB, bool STREAM = false>
+__device__ __forceinline__ double row_fold(double s, const int32_t* __restrict__ col,
+                                           const double* __restrict__ val, const double* x,
+                                           int64_t b, int64_t e) {
+  for (int64_t k = b; k < e; k += U) {
+    int32_t c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const bool ok = k + j < e;
+      // STREAM: operator entries of big levels are read once per sweep; the
+      // evict-first hint keeps them from displacing the L2-resident coarse levels
+      c[j] = ok ? (STREAM ? __ldcs(col + k + j) : col[k + j]) : 0;
+      v[j] = ok ? (STREAM ? __ldcs(val + k + j) : val[k + j]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = (k + j < e) ? x[c[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (k + j < e) s = SUB ? s - v[j] * xv[j] : s + v[j] * xv[j];
+  }
+  return s;
+}
+
+// THROUGHPUT-mode row dot product sum_k val[k] * x[col[k]] by a group of G
+// lanes: lane j takes k = b + j, b + j + G, ...; the partials meet in a
+// fixed xor-shuffle tree, so the result is deterministic (not the
+// sequential fold of VALIDATE mode). All lanes of the warp must call it;
+// lanes of invalid rows pass b == e. Every lane of the group gets the sum.
+template <int G, bool STREAM = false>
+__device__ __forceinline__ double group_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
+                                            const double* x, int64_t b, int64_t e) {
+  constexpr int U = 4;  // entries per lane per round, loads batched ahead of use
+  const int lane = threadIdx.x & (G - 1);
+  double p = 0.0;
+  for (int64_t k0 = b + lane; k0 < e; k0 += (int64_t)G * U) {
+    int32_t c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t k = k0 + (int64_t)j * G;
+      const bool ok = k < e;
+      c[j] = ok ? (STREAM ? __ldcs(col + k) : col[k]) : 0;
+      v[j] = ok ? (STREAM ? __ldcs(val + k) : val[k]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = (k0 + (int64_t)j * G < e) ? x[c[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) p += v[j] * xv[j];
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o, G);
+  return p;
+}
+
 // launches a kernel cooperatively (all blocks co-resident)
 void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** args, size_t smem = 0);
 

@@ -16,8 +16,7 @@ __global__ void residual_exact_kernel(CSRv a, const double* __restrict__ b,
   int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= a.n) return;
   double s = a.diag[u] * x[u];
-  const int64_t e = a.rp[u + 1];
-  for (int64_t k = a.rp[u]; k < e; ++k) s = s + a.val[k] * x[a.col[k]];
+  s = row_fold<8, false, true>(s, a.col, a.val, x, a.rp[u], a.rp[u + 1]);
   r[u] = b ? b[u] - s : s;
 }
 
@@ -141,7 +140,9 @@ __global__ void gs_fronts_kernel(CSRv a, const double* __restrict__ b, double* x
         const int32_t u = rows[i];
         double s = b ? b[(int64_t)u * K + kk] : 0.0;
         const int64_t e = a.rp[u + 1];
-        for (int64_t k = a.rp[u]; k < e; ++k) s = s - a.val[k] * x[(int64_t)a.col[k] * K + kk];
+        if (K == 1) s = row_fold<8, true>(s, a.col, a.val, x, a.rp[u], e);
+        else
+          for (int64_t k = a.rp[u]; k < e; ++k) s = s - a.val[k] * x[(int64_t)a.col[k] * K + kk];
         const double d = a.diag[u];
         if (d == 0.0) {
           if (e != a.rp[u])

@@ -52,7 +52,24 @@ struct DDirect {
   DVec<int64_t> lu_off;            // [ncomp] offsets into lu
   DVec<double> lu;                 // (cn+1)^2 row-major per component
   DVec<int32_t> perm;              // (cn+1) per component, offsets comp_start[c]+c
-  DVec<double> inv;                // throughput: first n columns of the inverse rows
+  DVec<double> inv;                // throughput: rows/cols [0,cn) of each bordered inverse
+  DVec<int64_t> inv_off;           // [ncomp] offsets into inv
+};
+
+// Throughput-mode smoother data: a greedy first-fit colouring in index order
+// (computed over the exact-order wavefronts, so it is the sequential greedy
+// colouring) and a copy of the operator whose rows are stored colour by
+// colour. A coloured sweep is a sequential sweep in colour-permuted order:
+// same hierarchy, different smoother.
+struct DColor {
+  int32_t ncolors = 0;
+  int group = 1;                // lanes per row in the throughput kernels (1, 4 or 8)
+  std::vector<int32_t> cptr_h;  // [ncolors+1] row ranges of each colour
+  DVec<int32_t> row_ids;        // natural row of each stored row
+  DVec<int64_t> rp;             // [n+1] permuted row pointers
+  DVec<int32_t> col;            // natural column indices
+  DVec<double> val;
+  DVec<double> diag;            // diag of each stored row
 };
 
 struct DLevel {
@@ -65,6 +82,7 @@ struct DLevel {
   int coarsest = CM_NONE;
   std::unique_ptr<DDirect> direct;
   Schedule sched;          // exact-order GS wavefronts of this level's operator
+  std::unique_ptr<DColor> color;  // throughput-mode coloured operator (on demand)
   UpperIndex upper;        // energy / relaxation helpers
 };
 
@@ -77,8 +95,7 @@ struct DHier {
   int device = 0;
   cudaStream_t owner_stream = nullptr;
   // throughput mode (colour-permuted copies), built on demand
-  struct Throughput* tp = nullptr;
-  ~DHier();
+  bool throughput_ready = false;
 };
 
 struct SetupOpts {
@@ -117,7 +134,19 @@ void galerkin(Ctx& c, const CSRv& a, const int32_t* agg, int32_t coarse_n, DCSR&
 void make_direct(Ctx& c, const CSRv& a, DDirect& d);
 // scratch: 2*maxN + 2 doubles
 void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exact, double* scratch);
-void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, double* x,
-                 DVec<double>& r, int* sweeps_out, bool exact);
+void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const double* b,
+                 double* x, DVec<double>& r, int* sweeps_out, bool exact);
+
+// throughput mode (throughput.cu)
+void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out);
+void gs_colored(Ctx& c, const DColor& col, int32_t n, const double* b, double* x, int sweeps);
+// throughput residual r = b - A x with `group` lanes per row (tree-folded rows)
+void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, int group);
+inline int row_group_for(int64_t n, int64_t m) {
+  const double deg = n ? 2.0 * (double)m / (double)n : 0.0;
+  return deg < 8.0 ? 1 : (deg < 24.0 ? 4 : 8);
+}
+void build_direct_inverse(Ctx& c, DDirect& d);
+void prepare_throughput(Ctx& c, DHier& h);
 
 }  // namespace lamgb

@@ -1122,7 +1122,7 @@ void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exa
     ++g_launches, direct_solve_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.lu_off.p, d.lu.p, d.perm.p,
                                             d.ncomp == 1, b, x, scratch, scratch + d.maxN + 1);
   } else {
-    ++g_launches, direct_inv_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.lu_off.p, d.inv.p,
+    ++g_launches, direct_inv_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.inv_off.p, d.inv.p,
                                           d.ncomp == 1, b, x);
   }
   CK_LAUNCH();
@@ -1131,8 +1131,8 @@ void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exa
 
 // RelaxationSolver::solve (coarse_solver.cpp:82-93); validate mode: exact-order
 // sweeps and sequential folds, one host check per sweep
-void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, double* x,
-                 DVec<double>& r, int* sweeps_out, bool exact) {
+void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const double* b,
+                 double* x, DVec<double>& r, int* sweeps_out, bool exact) {
   if (r.n < a.n) r.alloc(a.n, c.s);
   double* nrm = c.dscal + 110;
   residual_exact(c, a, b, x, r.p);
@@ -1143,7 +1143,8 @@ void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, do
   if (r0 == 0.0) return;
   const double target = 1e-12 * r0;
   for (int sweep = 0; sweep < 400; ++sweep) {
-    gs_exact(c, a, sch, b, x, 1, 1);
+    if (!exact && col) gs_colored(c, *col, a.n, b, x, 1);
+    else gs_exact(c, a, sch, b, x, 1, 1);
     c.work += (double)a.m;
     if (exact) subtract_mean_seq(c, x, a.n);
     else subtract_mean_tree(c, x, a.n);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "solve.cuh"
@@ -14,9 +15,6 @@
 namespace lamgb {
 
 uint64_t rng_derive_host(uint64_t seed, uint64_t stream);
-
-struct Throughput {};
-DHier::~DHier() { delete tp; }
 
 int LevelCredits::take(size_t l, double gamma) {
   if (credit.size() <= l) credit.resize(l + 1, 0.0);
@@ -48,6 +46,7 @@ static void prof_mark(Ctx& c, int cls, bool begin, double bytes = 0.0) {
 void Workspace::ensure(Ctx& c, const DHier& h) {
   if (owner == &h && lv.size() == h.levels.size()) return;
   owner = &h;
+  tail_built = false;
   lv.clear();
   lv.resize(h.levels.size());
   int32_t maxN = 0;
@@ -223,6 +222,10 @@ struct Driver {
   int relax_sweeps = 0;
 
   void visit(size_t l, const double* b, double* x, int theta) {
+    if (!exact && (int)l >= ws.tail.first) {
+      ws.tail.run(c, (int)l, theta, cfg.mu, (int)h.levels.size());
+      return;
+    }
     const DLevel& L = *h.levels[l];
     if (L.coarsest != CM_NONE) {
       coarsest(l, b, x);
@@ -238,7 +241,7 @@ struct Driver {
       direct_solve(c, *L.direct, b, x, exact, ws.direct_scratch.p);
     } else {
       int sw = 0;
-      relax_solve(c, L.op.view(), L.sched, b, x, ws.lv[l].r, &sw, exact);
+      relax_solve(c, L.op.view(), L.sched, L.color.get(), b, x, ws.lv[l].r, &sw, exact);
       relax_sweeps += sw;
     }
   }
@@ -285,7 +288,8 @@ struct Driver {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 0, true);
-    gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
+    if (!exact && L.color) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
+    else gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
     if (p) prof_mark(c, 0, false, (24.0 * L.op.m + 40.0 * L.op.n + 8.0) * sweeps);
     c.work += (double)L.op.m * sweeps;
   }
@@ -293,7 +297,8 @@ struct Driver {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
-    residual_exact(c, L.op.view(), b, x, r);
+    if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, L.color->group);
+    else residual_exact(c, L.op.view(), b, x, r);
     if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 40.0 * L.op.n + 8.0);
     c.work += (double)L.op.m;
   }
@@ -365,7 +370,10 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), c.s));
   ++g_launches, absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
   CK_LAUNCH();
-  seq_sum(c, b, n, bsum);
+  // the compatibility test is a threshold decision: sequential in VALIDATE
+  // mode (bit-exact with the reference), fixed-order tree otherwise
+  if (exact) seq_sum(c, b, n, bsum);
+  else tree_sum(c, b, n, bsum);
   CK(cudaMemcpyAsync(c.hscal, c.dscal + 140, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
   c.sync();
   double b_inf, b_sum = c.hscal[1];
@@ -377,11 +385,24 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   if (std::fabs(b_sum) > 1e-10 * b_inf)
     throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
 
+  if (!exact && !h.throughput_ready) {
+    prepare_throughput(c, const_cast<DHier&>(h));
+    const_cast<DHier&>(h).throughput_ready = true;
+  }
   if (!c.ws) c.ws = new Workspace();
   Workspace& ws = *c.ws;
   ws.ensure(c, h);
   ws.top_rhs_valid = false;
   if (cfg.correction == 1) ws.ensure_adaptive(c, h);
+  // the on-device tail needs the flat cycle (recombination stays host-driven)
+  const bool use_tail = !exact && cfg.correction == 0;
+  if (use_tail && !ws.tail_built) {
+    const char* env = getenv("LAMG_TAIL_ROWS");
+    ws.tail.build(c, h, ws, env ? atoi(env) : 20000);
+    ws.tail_built = true;
+  }
+  if (!use_tail) ws.tail.first = 1 << 30;
+  else ws.tail.reset(c);
   const double w0 = c.work = 0.0;
   copy_d(c, x, x0, n);
   double* rn_d = c.dscal + 150;
@@ -428,6 +449,8 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
     res.acf = std::pow(rp / r0, 1.0 / (double)res.cycles);
     res.solve_work = (c.work - w0) / (double)a.m;
   }
+  if (use_tail) ws.tail.collect(c, &c.work, &d.relax_sweeps);
+  if (use_tail) res.solve_work = (c.work - w0) / (double)a.m;
   res.recombinations = d.recombinations;
   res.recomb_max_growth = read_scalar(c, growth);
   res.relax_sweeps = d.relax_sweeps;

@@ -4,7 +4,7 @@
 #include <string>
 #include <vector>
 
-#include "hier.cuh"
+#include "tail.cuh"
 
 namespace lamgb {
 
@@ -48,6 +48,8 @@ struct Workspace {
   std::vector<LevelWS> lv;
   DVec<double> direct_scratch;
   bool top_rhs_valid = false;
+  TailPlan tail;          // throughput mode: on-device coarse tail
+  bool tail_built = false;
   void ensure(Ctx& c, const DHier& h);
   void ensure_adaptive(Ctx& c, const DHier& h);
 };

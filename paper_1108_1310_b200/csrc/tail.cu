@@ -1,0 +1,570 @@
+// tail.cu -- THROUGHPUT-mode coarse tail: one persistent cooperative kernel
+// runs the whole recursive sub-cycle (cycle.cpp:115-209) below a size
+// threshold.
+//
+// Coarse levels are small but visited geometrically often (gamma ~ 1.5 per
+// level), and a coloured sweep is ~10 dependent colour phases. Host-driven,
+// every phase is a kernel launch. Here the recursion, the per-level credits
+// (LevelCredit::take, cycle.cpp:14-21) and every transfer run on the device:
+//  - mid-size levels use the whole grid, a phase costs one grid barrier;
+//  - levels of at most `small_rows` rows (and their whole subtree) run in
+//    CTA 0 alone, a phase costs a __syncthreads, and the coloured operator,
+//    x and b of a level are staged in shared memory for its sweeps.
+// Every thread runs the same control flow on its own frame stack; credits
+// live in shared memory (identical in every CTA for the mid levels).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "solve.cuh"
+
+namespace lamgb {
+
+namespace {
+
+constexpr int kTailThreads = 512;
+
+struct BlockScope {
+  __device__ static int64_t tid() { return threadIdx.x; }
+  __device__ static int64_t stride() { return blockDim.x; }
+  __device__ static void sync() { __syncthreads(); }
+  __device__ static bool leader() { return threadIdx.x == 0; }
+};
+struct GridScope {
+  __device__ static int64_t tid() { return blockIdx.x * (int64_t)blockDim.x + threadIdx.x; }
+  __device__ static int64_t stride() { return (int64_t)gridDim.x * blockDim.x; }
+  __device__ static void sync() { cg::this_grid().sync(); }
+  __device__ static bool leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
+};
+
+// ---------------------------------------------------------------- sweeps
+// shared-memory sweep (BlockScope only): every load of the sweep is an LDS
+__device__ inline void gs_smem(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
+                               TailCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const long long t0 = clock64();
+  const int32_t n = L.n;
+  const int64_t nnz = 2 * L.m;
+  double* s_x = (double*)smem;
+  double* s_b = s_x + n;
+  double* s_d = s_b + n;
+  double* s_v = s_d + n;
+  int32_t* s_c = (int32_t*)(s_v + nnz);
+  int32_t* s_rp = s_c + nnz;
+  int32_t* s_id = s_rp + n + 1;
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int32_t u = L.row_ids[i];
+    const double xi = x[i], di = L.pdiag[i];
+    const int32_t ri = (int32_t)L.prp[i];
+    s_x[i] = xi;
+    s_id[i] = u;
+    s_d[i] = di;
+    s_rp[i] = ri;
+    s_b[i] = b[u];
+  }
+  if (threadIdx.x == 0) s_rp[n] = (int32_t)L.prp[n];
+  for (int64_t k0 = threadIdx.x; k0 < nnz; k0 += 4 * (int64_t)blockDim.x) {
+    int32_t cv[4];
+    double vv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t k = k0 + (int64_t)j * blockDim.x;
+      cv[j] = k < nnz ? L.pcol[k] : 0;
+      vv[j] = k < nnz ? L.pval[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t k = k0 + (int64_t)j * blockDim.x;
+      if (k < nnz) {
+        s_c[k] = cv[j];
+        s_v[k] = vv[j];
+      }
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  // G = 4 lanes per row, tree-folded (deterministic)
+  constexpr int G = 4;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int32_t cc = 0; cc < L.ncolors; ++cc) {
+      const int32_t i0 = L.cptr[cc], i1 = L.cptr[cc + 1];
+      const int32_t span = ((i1 - i0) * G + 31) / 32 * 32;
+      for (int32_t t = threadIdx.x; t < span; t += blockDim.x) {
+        const int32_t i = i0 + t / G;
+        const bool ok = i < i1;
+        const int lane = t & (G - 1);
+        double p = 0.0;
+        if (ok) {
+          const int32_t e = s_rp[i + 1];
+          for (int32_t k = s_rp[i] + lane; k < e; k += G) p += s_v[k] * s_x[s_c[k]];
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o, G);
+        if (ok && lane == 0) s_x[s_id[i]] = (s_b[i] - p) / s_d[i];
+      }
+      __syncthreads();
+    }
+  const long long t2 = clock64();
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = s_x[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctr->smem_calls += 1;
+    ctr->smem_phases += (long long)sweeps * L.ncolors;
+    ctr->cyc_stage += (t1 - t0) + (clock64() - t2);
+    ctr->cyc_phases += t2 - t1;
+  }
+}
+
+template <class S, int G>
+__device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, double* x, int sweeps) {
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int32_t cc = 0; cc < L.ncolors; ++cc) {
+      const int32_t i0 = L.cptr[cc], i1 = L.cptr[cc + 1];
+      // whole warps iterate together (the group shuffles need every lane)
+      const int64_t span = ((int64_t)(i1 - i0) * G + 31) / 32 * 32;
+      for (int64_t t = S::tid(); t < span; t += S::stride()) {
+        const int64_t i = i0 + t / G;
+        const bool ok = i < i1;
+        if (G == 1) {
+          if (ok) {
+            const int32_t u = L.row_ids[i];
+            x[u] = row_fold<8, true>(b[u], L.pcol, L.pval, x, L.prp[i], L.prp[i + 1]) / L.pdiag[i];
+          }
+        } else {
+          const double dot = group_dot<G>(L.pcol, L.pval, x, ok ? L.prp[i] : 0, ok ? L.prp[i + 1] : 0);
+          if (ok && (threadIdx.x & (G - 1)) == 0) {
+            const int32_t u = L.row_ids[i];
+            x[u] = (b[u] - dot) / L.pdiag[i];
+          }
+        }
+      }
+      S::sync();
+    }
+}
+
+template <class S>
+__device__ inline void gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps, TailCounters* ctr) {
+  if (L.ncolors == 0 || sweeps == 0) return;
+  if (S::leader()) ctr->phases += (long long)sweeps * L.ncolors;
+  if (!std::is_same<S, GridScope>::value && L.smem_ok) {
+    gs_smem(L, b, x, sweeps, ctr);
+    return;
+  }
+  const long long tg = clock64();
+  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps);
+  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps);
+  else gs_group<S, 1>(L, b, x, sweeps);
+  if (S::leader()) {
+    ctr->cyc_global_gs += clock64() - tg;
+    ctr->global_phases += (long long)sweeps * L.ncolors;
+  }
+}
+
+// -------------------------------------------------------------- transfers
+template <class S, int G>
+__device__ inline void residual_group(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
+  const int64_t span = ((int64_t)L.n * G + 31) / 32 * 32;
+  for (int64_t t = S::tid(); t < span; t += S::stride()) {
+    const int64_t u = t / G;
+    const bool ok = u < L.n;
+    if (G == 1) {
+      if (ok) {
+        double s = L.diag[u] * x[u];
+        s = row_fold<8, false>(s, L.col, L.val, x, L.rp[u], L.rp[u + 1]);
+        r[u] = b[u] - s;
+      }
+    } else {
+      const double dot = group_dot<G>(L.col, L.val, x, ok ? L.rp[u] : 0, ok ? L.rp[u + 1] : 0);
+      if (ok && (threadIdx.x & (G - 1)) == 0) r[u] = b[u] - (L.diag[u] * x[u] + dot);
+    }
+  }
+  S::sync();
+}
+
+template <class S>
+__device__ inline void residual(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
+  if (L.group == 8) residual_group<S, 8>(L, b, x, r);
+  else if (L.group == 4) residual_group<S, 4>(L, b, x, r);
+  else residual_group<S, 1>(L, b, x, r);
+}
+
+// restrict r into the child's rhs (member-ordered fold, times mu) and zero
+// the child's iterate
+template <class S>
+__device__ inline void restrict_to(const TLevel& L, const TLevel& C, const double* r, double mu) {
+  for (int64_t g = S::tid(); g < C.n; g += S::stride()) {
+    double s = 0.0;
+    for (int64_t j = L.mem_ptr[g]; j < L.mem_ptr[g + 1]; ++j) s = s + r[L.mem[j]];
+    C.b[g] = mu != 1.0 ? s * mu : s;
+    C.x[g] = 0.0;
+  }
+  S::sync();
+}
+
+template <class S>
+__device__ inline void interpolate(const TLevel& L, const TLevel& C, double* x) {
+  for (int64_t u = S::tid(); u < L.n; u += S::stride()) x[u] = x[u] + C.x[L.agg[u]];
+  S::sync();
+}
+
+template <class S>
+__device__ inline void coarsen(const StageV& s, const double* b, double* bc) {
+  for (int64_t k = S::tid(); k < s.coarse_n; k += S::stride()) {
+    double v = b[s.poc[k]];
+    for (int64_t j = s.t_ptr[k]; j < s.t_ptr[k + 1]; ++j) {
+      const int64_t p = s.t_p[j];
+      const int32_t i = s.f_of_p[p];
+      v = v - s.f_val[p] * (b[s.f_nodes[i]] / s.f_diag[i]);
+    }
+    bc[k] = v;
+  }
+  S::sync();
+}
+
+template <class S>
+__device__ inline void inject(const StageV& s, const double* x, double* xc) {
+  for (int64_t k = S::tid(); k < s.coarse_n; k += S::stride()) xc[k] = x[s.poc[k]];
+  S::sync();
+}
+
+template <class S>
+__device__ inline void backsub(const StageV& s, const double* xc, const double* b, double* x) {
+  for (int64_t k = S::tid(); k < s.coarse_n; k += S::stride()) x[s.poc[k]] = xc[k];
+  S::sync();
+  for (int64_t i = S::tid(); i < s.nf; i += S::stride()) {
+    const int32_t f = s.f_nodes[i];
+    double sum = b[f];
+    for (int64_t p = s.f_ptr[i]; p < s.f_ptr[i + 1]; ++p) sum = sum - s.f_val[p] * x[s.f_nbr[p]];
+    x[f] = sum / s.f_diag[i];
+  }
+  S::sync();
+}
+
+// x = Minv[:n,:n] b per component: one warp per row, fixed-order lane folds
+// (the coarsest level always runs in one CTA)
+__device__ inline void direct(const TLevel& L, const double* b, double* x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int32_t ci = 0; ci < L.ncomp; ++ci) {
+    const int32_t s0 = L.comp_start[ci], cn = L.comp_start[ci + 1] - s0;
+    const double* Mi = L.inv + L.inv_off[ci];
+    for (int32_t i = warp; i < cn; i += nw) {
+      double s = 0.0;
+      for (int32_t j = lane; j < cn; j += 32) s += Mi[(int64_t)i * cn + j] * (L.whole ? b[j] : b[L.nodes[s0 + j]]);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        if (L.whole) x[i] = s;
+        else x[L.nodes[s0 + i]] = s;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// fixed-order reduction over the scope; every thread gets the same value
+template <class S>
+__device__ inline double scope_sum(double v, double* sh, double* part) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    sh[32] = t;
+    if (std::is_same<S, GridScope>::value) part[blockIdx.x] = t;
+  }
+  S::sync();
+  double t = sh[32];
+  if (std::is_same<S, GridScope>::value) {
+    t = 0.0;
+    for (unsigned g = 0; g < gridDim.x; ++g) t += ((volatile double*)part)[g];
+  }
+  S::sync();
+  return t;
+}
+
+// RelaxationSolver::solve (coarse_solver.cpp:82-93)
+template <class S>
+__device__ inline void relax(const TLevel& L, const double* b, double* x, double* sh, double* part,
+                             TailCounters* ctr) {
+  residual<S>(L, b, x, L.r);
+  double loc = 0.0;
+  for (int64_t u = S::tid(); u < L.n; u += S::stride()) loc += L.r[u] * L.r[u];
+  const double r0 = sqrt(scope_sum<S>(loc, sh, part));
+  if (S::leader()) ctr->work += (double)L.m;
+  if (r0 == 0.0) return;
+  const double target = 1e-12 * r0;
+  for (int sweep = 0; sweep < 400; ++sweep) {
+    gs<S>(L, b, x, 1, ctr);
+    loc = 0.0;
+    for (int64_t u = S::tid(); u < L.n; u += S::stride()) loc += x[u];
+    const double mean = scope_sum<S>(loc, sh, part) / (double)L.n;
+    for (int64_t u = S::tid(); u < L.n; u += S::stride()) x[u] = x[u] - mean;
+    S::sync();
+    residual<S>(L, b, x, L.r);
+    loc = 0.0;
+    for (int64_t u = S::tid(); u < L.n; u += S::stride()) loc += L.r[u] * L.r[u];
+    const double rn = sqrt(scope_sum<S>(loc, sh, part));
+    if (S::leader()) {
+      ctr->work += 2.0 * (double)L.m;
+      ctr->relax_sweeps += 1;
+    }
+    if (rn <= target) break;
+  }
+}
+
+struct Frame {
+  int l, theta, it, step;
+};
+
+// LevelCredit::take on the CTA's shared credits
+__device__ inline int take(double* credits, int l, double gamma) {
+  double cr = credits[l] + gamma;
+  int th = (int)floor(cr);
+  if (th < 1) th = 1;
+  cr -= th;
+  if (cr < 0.0) cr = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) credits[l] = cr;
+  __syncthreads();
+  return th;
+}
+
+template <class S>
+__device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
+                           int32_t small_rows, double* sh, double* part, TailCounters* ctr);
+
+// CTA 0 runs a small subtree alone; the other CTAs wait at the grid barrier
+__device__ inline bool small_handoff(const TLevel* levels, const Frame& f, double* credits, double mu,
+                                     int32_t small_rows, double* sh, double* part, TailCounters* ctr) {
+  if (levels[f.l].n > small_rows) return false;
+  if (blockIdx.x == 0) visit_loop<BlockScope>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr);
+  GridScope::sync();
+  return true;
+}
+
+template <class S>
+__device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
+                           int32_t small_rows, double* sh, double* part, TailCounters* ctr) {
+  Frame st[kMaxLevels];
+  int sp = 0;
+  st[sp++] = Frame{l0, theta0, 0, 0};
+  while (sp > 0) {
+    Frame& f = st[sp - 1];
+    if (std::is_same<S, GridScope>::value && f.step == 0 && f.it == 0 &&
+        small_handoff(levels, f, credits, mu, small_rows, sh, part, ctr)) {
+      --sp;
+      continue;
+    }
+    const TLevel& L = levels[f.l];
+    if (L.coarsest == CM_DIRECT) {
+      direct(L, L.b, L.x);
+      if (S::leader()) ctr->work += (double)L.m;
+      --sp;
+      continue;
+    }
+    if (L.coarsest == CM_RELAX) {
+      relax<S>(L, L.b, L.x, sh, part, ctr);
+      --sp;
+      continue;
+    }
+    const TLevel& C = levels[f.l + 1];
+    if (L.child_kind == KIND_AGG) {
+      if (f.step == 0) {
+        if (f.it == f.theta) {
+          --sp;
+          continue;
+        }
+        if (C.nu_pre) gs<S>(L, L.b, L.x, C.nu_pre, ctr);
+        residual<S>(L, L.b, L.x, L.r);
+        restrict_to<S>(L, C, L.r, mu);
+        if (S::leader()) ctr->work += (double)L.m * (C.nu_pre + 1);
+        const int th = take(credits, f.l + 1, C.gamma);
+        f.step = 1;
+        st[sp++] = Frame{f.l + 1, th, 0, 0};
+      } else {
+        interpolate<S>(L, C, L.x);
+        if (C.nu_post) gs<S>(L, L.b, L.x, C.nu_post, ctr);
+        if (S::leader()) ctr->work += (double)L.m * C.nu_post;
+        ++f.it;
+        f.step = 0;
+      }
+    } else {  // elimination child (cycle.cpp:131-164)
+      if (f.step == 0) {
+        if (f.it == 0) {
+          const double* in = L.b;
+          for (int s = 0; s < L.nstages; ++s) {
+            double* out = s + 1 < L.nstages ? L.stage_rhs[s + 1] : C.b;
+            coarsen<S>(L.stages[s], in, out);
+            in = out;
+          }
+          if (S::leader()) ctr->work += (double)L.elim_nnz;
+        }
+        if (f.it == f.theta) {
+          --sp;
+          continue;
+        }
+        const double* cur = L.x;
+        for (int s = 0; s < L.nstages; ++s) {
+          double* out = s + 1 < L.nstages ? L.stage_x[s + 1] : C.x;
+          inject<S>(L.stages[s], cur, out);
+          cur = out;
+        }
+        const int th = take(credits, f.l + 1, C.gamma);
+        f.step = 1;
+        st[sp++] = Frame{f.l + 1, th, 0, 0};
+      } else {
+        for (int s = L.nstages; s-- > 0;) {
+          const double* xc = s + 1 < L.nstages ? L.stage_x[s + 1] : C.x;
+          double* out = s == 0 ? L.x : L.stage_x[s];
+          const double* rhs = s == 0 ? L.b : L.stage_rhs[s];
+          backsub<S>(L.stages[s], xc, rhs, out);
+        }
+        if (S::leader()) ctr->work += (double)L.elim_nnz;
+        ++f.it;
+        f.step = 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTailThreads) tail_kernel(const TLevel* __restrict__ levels, int nlevels, int l0,
+                                                            int theta0, double* credits_g, double mu,
+                                                            int32_t small_rows, double* part, TailCounters* ctr) {
+  __shared__ double credits[kMaxLevels];
+  __shared__ double sh[64];
+  const long long t_start = clock64();
+  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = credits_g[l];
+  __syncthreads();
+  visit_loop<GridScope>(levels, l0, theta0, credits, mu, small_rows, sh, part, ctr);
+  if (blockIdx.x == 0) {
+    for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits_g[l] = credits[l];
+    if (threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
+  }
+}
+
+}  // namespace
+
+void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
+  const int nl = (int)h.levels.size();
+  first = nl;  // no tail
+  for (int l = 1; l < nl; ++l)
+    if (h.levels[l]->op.n <= max_rows) {
+      first = l;
+      break;
+    }
+  if (first >= nl || nl > kMaxLevels) {
+    first = 1 << 30;
+    return;
+  }
+  const char* e1 = getenv("LAMG_TAIL_SMALL");
+  small_rows = e1 ? atoi(e1) : 4096;
+  const char* e2 = getenv("LAMG_TAIL_CTAS");
+  ctas = std::max(1, std::min(e2 ? atoi(e2) : 64, c.sms));
+  std::vector<TLevel> tl(nl);
+  for (int l = first; l < nl; ++l) {
+    const DLevel& L = *h.levels[l];
+    TLevel& t = tl[l];
+    memset(&t, 0, sizeof t);
+    const CSRv a = L.op.view();
+    t.n = a.n;
+    t.m = a.m;
+    t.rp = a.rp;
+    t.col = a.col;
+    t.val = a.val;
+    t.diag = a.diag;
+    t.b = ws.lv[l].b.p;
+    t.x = ws.lv[l].x.p;
+    t.r = ws.lv[l].r.p;
+    t.gamma = L.gamma;
+    t.nu_pre = L.nu_pre;
+    t.nu_post = L.nu_post;
+    t.coarsest = L.coarsest;
+    t.group = row_group_for(a.n, a.m);
+    if (L.color) {
+      t.ncolors = L.color->ncolors;
+      t.cptr = (const int32_t*)(L.color->rp.p + a.n + 1);
+      t.row_ids = L.color->row_ids.p;
+      t.prp = L.color->rp.p;
+      t.pcol = L.color->col.p;
+      t.pval = L.color->val.p;
+      t.pdiag = L.color->diag.p;
+      const int64_t bytes = (int64_t)a.n * (3 * 8 + 4 + 4) + 4 + 2 * a.m * 12;
+      t.smem_ok = bytes <= kTailSmem;
+    }
+    if (L.direct) {
+      const DDirect& d = *L.direct;
+      t.ncomp = d.ncomp;
+      t.comp_start = d.comp_start.p;
+      t.nodes = d.nodes.p;
+      t.inv = d.inv.p;
+      t.inv_off = d.inv_off.p;
+      t.whole = d.ncomp == 1;
+      if (a.n > small_rows) small_rows = a.n;  // the direct coarsest runs in one CTA
+    }
+    if (l + 1 < nl && L.coarsest == CM_NONE) {
+      const DLevel& C = *h.levels[l + 1];
+      t.child_kind = C.kind;
+      if (C.kind == KIND_AGG) {
+        t.agg = C.agg->aggregate_of.p;
+        t.mem_ptr = C.agg->mem_ptr.p;
+        t.mem = C.agg->mem.p;
+      } else {
+        t.nstages = (int)C.stages.size();
+        if (t.nstages > kMaxStages) throw LamgError(LAMG_E_ERROR, "tail: too many elimination stages");
+        for (int s = 0; s < t.nstages; ++s) {
+          t.stages[s] = C.stages[s]->view();
+          t.elim_nnz += C.stages[s]->nnzf;
+          if (s >= 1) {
+            t.stage_rhs[s] = ws.lv[l].stage_rhs[s].p;
+            t.stage_x[s] = ws.lv[l].stage_x[s].p;
+          }
+        }
+      }
+    }
+  }
+  dlevels.alloc(nl, c.s);
+  CK(cudaMemcpyAsync(dlevels.p, tl.data(), sizeof(TLevel) * nl, cudaMemcpyHostToDevice, c.s));
+  credits.alloc(nl, c.s);
+  ctr.alloc(1, c.s);
+  CK(cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_kernel, kTailThreads, kTailSmem));
+  ctas = std::min(ctas, std::max(1, per_sm) * c.sms);
+  part.alloc(std::max(ctas, 1), c.s);
+  c.sync();
+}
+
+void TailPlan::reset(Ctx& c) {
+  if (!credits.n) return;
+  credits.zero();
+  ctr.zero();
+}
+
+void TailPlan::run(Ctx& c, int l, int theta, double mu, int nlevels) {
+  const TLevel* lv = dlevels.p;
+  double* cr = credits.p;
+  double* pt = part.p;
+  TailCounters* ct = ctr.p;
+  int32_t sr = small_rows;
+  void* args[] = {(void*)&lv, &nlevels, &l, &theta, &cr, &mu, &sr, &pt, &ct};
+  coop_launch(c, (const void*)tail_kernel, ctas, kTailThreads, args, kTailSmem);
+}
+
+void TailPlan::collect(Ctx& c, double* work, int* relax_sweeps) {
+  if (!ctr.n) return;
+  TailCounters h;
+  CK(cudaMemcpyAsync(&h, ctr.p, sizeof h, cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  *work += h.work;
+  *relax_sweeps += (int)h.relax_sweeps;
+  if (getenv("LAMG_TAIL_DEBUG"))
+    fprintf(stderr,
+            "[tail] first %d ctas %d small %d: phases %lld, %lld cycles in tail kernels; smem: %lld calls %lld "
+            "phases, stage %.0f cyc/call, %.0f cyc/phase; global gs: %lld phases %.0f cyc/phase\n",
+            first, ctas, small_rows, h.phases, h.cyc_total, h.smem_calls, h.smem_phases,
+            h.smem_calls ? (double)h.cyc_stage / h.smem_calls : 0.0,
+            h.smem_phases ? (double)h.cyc_phases / h.smem_phases : 0.0, h.global_phases,
+            h.global_phases ? (double)h.cyc_global_gs / h.global_phases : 0.0);
+}
+
+}  // namespace lamgb

@@ -1,0 +1,84 @@
+// tail.cuh -- device descriptors for the single-CTA coarse-tail kernel.
+#pragma once
+
+#include <type_traits>
+
+#include "hier.cuh"
+
+namespace lamgb {
+
+constexpr int kMaxLevels = 64;
+constexpr int kMaxStages = 8;
+constexpr int kTailSmem = 200 * 1024;  // dynamic shared memory of the tail CTA
+
+struct TailCounters {
+  double work;          // edge units (exact integers: order-free)
+  long long relax_sweeps;
+  long long phases;     // diagnostics: colour phases, total cycles, GS cycles
+  long long cyc_total, cyc_gs;
+  long long smem_calls, smem_phases, cyc_stage, cyc_phases, cyc_global_gs, global_phases;
+};
+
+// one level as the tail kernel sees it: operator (natural + colour-permuted),
+// the transfer to its child, and its workspace vectors
+struct TLevel {
+  int32_t n;
+  int64_t m;
+  const int64_t* rp;
+  const int32_t* col;
+  const double* val;
+  const double* diag;
+  // coloured copy (GS)
+  int32_t ncolors;
+  const int32_t* cptr;
+  const int32_t* row_ids;
+  const int64_t* prp;
+  const int32_t* pcol;
+  const double* pval;
+  const double* pdiag;
+  int group;    // lanes per row (1, 4, 8)
+  int smem_ok;  // the coloured operator + x + b fit the tail CTA's shared memory
+  // workspace
+  double* b;
+  double* x;
+  double* r;
+  // solve parameters the parent uses when visiting this level
+  double gamma;
+  int nu_pre, nu_post;
+  int coarsest;
+  // coarsest direct (throughput inverse)
+  int32_t ncomp;
+  const int32_t* comp_start;
+  const int32_t* nodes;
+  const double* inv;
+  const int64_t* inv_off;
+  int whole;
+  // transfer to the child level
+  int child_kind;
+  const int32_t* agg;
+  const int64_t* mem_ptr;
+  const int32_t* mem;
+  int nstages;
+  int64_t elim_nnz;
+  StageV stages[kMaxStages];
+  double* stage_rhs[kMaxStages];
+  double* stage_x[kMaxStages];
+};
+
+struct Workspace;
+
+struct TailPlan {
+  int first = 1 << 30;  // first level handled on-device (>= nlevels: none)
+  int32_t small_rows = 4096;  // levels this small run in CTA 0 alone
+  int ctas = 64;
+  DVec<TLevel> dlevels;
+  DVec<double> credits;
+  DVec<double> part;
+  DVec<TailCounters> ctr;
+  void build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows);
+  void reset(Ctx& c);
+  void run(Ctx& c, int l, int theta, double mu, int nlevels);
+  void collect(Ctx& c, double* work, int* relax_sweeps);
+};
+
+}  // namespace lamgb

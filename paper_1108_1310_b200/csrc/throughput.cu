@@ -1,0 +1,278 @@
+// throughput.cu -- THROUGHPUT-mode smoother: greedy colouring, colour-
+// permuted operator copies, coloured Gauss-Seidel, and the coarsest inverse.
+//
+// The hierarchy (every integer artefact and coarse value) is the bit-exact
+// VALIDATE-mode one; only the solve's smoother order and its reductions
+// change.
+#include <algorithm>
+
+#include "hier.cuh"
+
+namespace lamgb {
+
+// First-fit colour in index order: u takes the smallest colour unused by its
+// lower neighbours. Lower neighbours sit in earlier wavefronts, so walking
+// the exact-order fronts reproduces the sequential greedy colouring.
+__global__ void color_fronts_kernel(CSRv a, const int32_t* __restrict__ front_ptr,
+                                    const int32_t* __restrict__ rows, int32_t nfronts, int32_t* color) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t f = 0; f < nfronts; ++f) {
+    for (int64_t i = front_ptr[f] + gtid; i < front_ptr[f + 1]; i += gstride) {
+      const int32_t u = rows[i];
+      int32_t base = 0;
+      while (true) {
+        unsigned long long used = 0ull;
+        for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
+          int32_t v = a.col[k];
+          if (v >= u) break;  // rows are sorted: lower neighbours first
+          int32_t cv = ((volatile int32_t*)color)[v] - base;
+          if (cv >= 0 && cv < 64) used |= 1ull << cv;
+        }
+        if (~used) {
+          color[u] = base + __ffsll((long long)~used) - 1;
+          break;
+        }
+        base += 64;
+      }
+    }
+    grid_barrier();
+  }
+}
+
+__global__ void iota32_kernel(int32_t* x, int32_t n) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+__global__ void color_bounds_kernel(const uint32_t* sorted, int32_t n, int32_t ncol, int32_t* cptr) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  int32_t lo = i == 0 ? 0 : (int32_t)sorted[i - 1] + 1;
+  int32_t hi = i == n ? ncol : (int32_t)sorted[i];
+  for (int32_t k = lo; k <= hi && k <= ncol; ++k) cptr[k] = i;
+}
+__global__ void perm_deg_kernel(CSRv a, const int32_t* row_ids, int64_t* deg) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int32_t u = row_ids[i];
+  deg[i] = a.rp[u + 1] - a.rp[u];
+}
+__global__ void perm_fill_kernel(CSRv a, const int32_t* row_ids, const int64_t* prp, int32_t* pcol,
+                                 double* pval, double* pdiag) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int32_t u = row_ids[i];
+  int64_t o = prp[i];
+  for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k, ++o) {
+    pcol[o] = a.col[k];
+    pval[o] = a.val[k];
+  }
+  pdiag[i] = a.diag[u];
+}
+
+void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
+  const int32_t n = a.n;
+  DVec<int32_t> color(n, c.s);
+  color.fill_bytes(0xff);  // -1: not yet coloured
+  const int threads = 256;
+  int blocks = (int)std::min<int64_t>(c.max_coop_blocks((const void*)color_fronts_kernel, threads),
+                                      std::max<int64_t>(1, (sch.max_width + threads - 1) / threads));
+  if (sch.max_width <= 2 * threads) blocks = 1;
+  CSRv av = a;
+  const int32_t* fp = sch.front_ptr.p;
+  const int32_t* rw = sch.rows.p;
+  int32_t nf = sch.nfronts;
+  void* args[] = {&av, (void*)&fp, (void*)&rw, &nf, &color.p};
+  coop_launch(c, (const void*)color_fronts_kernel, blocks, threads, args);
+  const int32_t ncol = reduce_max_i32(c, color.p, n) + 1;
+  DVec<int32_t> ids(n, c.s);
+  DVec<uint32_t> ks(n, c.s);
+  ++g_launches, iota32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
+  CK_LAUNCH();
+  out.row_ids.alloc(n, c.s);
+  int bits = 1;
+  while ((1 << bits) <= ncol && bits < 31) ++bits;
+  sort_pairs_u32_i32(c, (const uint32_t*)color.p, ks.p, ids.p, out.row_ids.p, n, bits);
+  DVec<int32_t> cptr(ncol + 1, c.s);
+  ++g_launches, color_bounds_kernel<<<blocks_for(n + 1), kThreads, 0, c.s>>>(ks.p, n, ncol, cptr.p);
+  CK_LAUNCH();
+  out.ncolors = ncol;
+  out.group = row_group_for(a.n, a.m);
+  out.cptr_h = cptr.to_host();
+  DVec<int64_t> deg(n + 1, c.s);
+  ++g_launches, perm_deg_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, deg.p);
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), c.s));
+  out.rp.alloc(n + 1, c.s);
+  exclusive_scan_i64(c, deg.p, out.rp.p, n + 1);
+  out.col.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
+  out.val.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
+  out.diag.alloc(n, c.s);
+  ++g_launches, perm_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
+                                                                     out.val.p, out.diag.p);
+  CK_LAUNCH();
+}
+
+// One colour: rows [i0, i1) of the permuted operator update in parallel.
+__global__ void gs_color_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const double* __restrict__ val, const double* __restrict__ diag,
+                                const int32_t* __restrict__ row_ids, const double* __restrict__ b,
+                                double* x, int32_t i0, int32_t i1) {
+  int32_t i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  const int32_t u = row_ids[i];
+  double s = row_fold<8, true, true>(b[u], col, val, x, rp[i], rp[i + 1]);
+  x[u] = s / diag[i];
+}
+
+// One colour with G lanes per row (coarse levels: rows of ~10-40 entries
+// would otherwise serialise their loads in one thread).
+template <int G>
+__global__ void gs_color_group_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                      const double* __restrict__ val, const double* __restrict__ diag,
+                                      const int32_t* __restrict__ row_ids, const double* __restrict__ b,
+                                      double* x, int32_t i0, int32_t i1) {
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t i = i0 + gid;
+  const bool ok = i < i1;
+  const double dot = group_dot<G>(col, val, x, ok ? rp[i] : 0, ok ? rp[i + 1] : 0);
+  if (ok && (threadIdx.x & (G - 1)) == 0) {
+    const int32_t u = row_ids[i];
+    x[u] = (b[u] - dot) / diag[i];
+  }
+}
+
+template <int G>
+__global__ void residual_group_kernel(CSRv a, const double* __restrict__ b, const double* __restrict__ x,
+                                      double* __restrict__ r) {
+  const int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const bool ok = u < a.n;
+  const double dot = group_dot<G>(a.col, a.val, x, ok ? a.rp[u] : 0, ok ? a.rp[u + 1] : 0);
+  if (ok && (threadIdx.x & (G - 1)) == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
+}
+
+void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, int group) {
+  if (a.n == 0) return;
+  if (group == 1) {
+    residual_exact(c, a, b, x, r);
+    return;
+  }
+  const int64_t threads = (int64_t)a.n * group;
+  if (group == 4) ++g_launches, residual_group_kernel<4><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
+  else ++g_launches, residual_group_kernel<8><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
+  CK_LAUNCH();
+}
+
+// All colours and sweeps of a small level in one CTA (no launch per colour).
+__global__ void gs_color_cta_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                    const double* __restrict__ val, const double* __restrict__ diag,
+                                    const int32_t* __restrict__ row_ids, const int32_t* __restrict__ cptr,
+                                    int32_t ncolors, const double* __restrict__ b, double* x, int sweeps) {
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int32_t cc = 0; cc < ncolors; ++cc) {
+      for (int32_t i = cptr[cc] + threadIdx.x; i < cptr[cc + 1]; i += blockDim.x) {
+        const int32_t u = row_ids[i];
+        double s = row_fold<8, true>(b[u], col, val, x, rp[i], rp[i + 1]);
+        x[u] = s / diag[i];
+      }
+      __syncthreads();
+    }
+}
+
+void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x, int sweeps) {
+  if (n == 0 || sweeps <= 0) return;
+  if (n <= 16384) {
+    // device copy of the colour pointers lives right after the permuted rp
+    static_assert(sizeof(int64_t) >= sizeof(int32_t), "");
+    ++g_launches, gs_color_cta_kernel<<<1, 1024, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
+                                                           (const int32_t*)(cl.rp.p + n + 1), cl.ncolors, b, x,
+                                                           sweeps);
+    CK_LAUNCH();
+    return;
+  }
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int32_t cc = 0; cc < cl.ncolors; ++cc) {
+      int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
+      if (i1 <= i0) continue;
+      const int64_t rows = i1 - i0;
+      if (cl.group == 1)
+        ++g_launches, gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
+                                                                             cl.row_ids.p, b, x, i0, i1);
+      else if (cl.group == 4)
+        ++g_launches, gs_color_group_kernel<4><<<blocks_for(rows * 4), kThreads, 0, c.s>>>(
+            cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
+      else
+        ++g_launches, gs_color_group_kernel<8><<<blocks_for(rows * 8), kThreads, 0, c.s>>>(
+            cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
+    }
+  CK_LAUNCH();
+}
+
+// Rows [0, cn) of the inverse of each bordered LU factor: x = Minv[:cn,:cn] b
+// (rhs[cn] = 0). One thread per unit right-hand side.
+__global__ void lu_inverse_kernel(const double* M, const int32_t* perm, int32_t N, double* inv, double* work) {
+  int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t cn = N - 1;
+  if (j >= cn) return;
+  double* y = work + (int64_t)j * N;
+  for (int32_t i = 0; i < N; ++i) {
+    double s = perm[i] == j ? 1.0 : 0.0;
+    for (int32_t k = 0; k < i; ++k) s -= M[(int64_t)i * N + k] * y[k];
+    y[i] = s;
+  }
+  for (int32_t i = N; i-- > 0;) {
+    double s = y[i];
+    for (int32_t k = i + 1; k < N; ++k) s -= M[(int64_t)i * N + k] * y[k];
+    y[i] = s / M[(int64_t)i * N + i];
+  }
+  for (int32_t i = 0; i < cn; ++i) inv[(int64_t)i * cn + j] = y[i];
+}
+
+void build_direct_inverse(Ctx& c, DDirect& d) {
+  if (d.inv.n) return;
+  std::vector<int64_t> off = d.lu_off.to_host();
+  std::vector<int32_t> start = d.comp_start.to_host();
+  int64_t total = 0;
+  std::vector<int64_t> ioff(d.ncomp);
+  for (int32_t ci = 0; ci < d.ncomp; ++ci) {
+    ioff[ci] = total;
+    total += (int64_t)d.comp_size[ci] * d.comp_size[ci];
+  }
+  d.inv.alloc(std::max<int64_t>(total, 1), c.s);
+  DVec<double> work((int64_t)d.maxN * d.maxN + 1, c.s);
+  for (int32_t ci = 0; ci < d.ncomp; ++ci) {
+    const int32_t N = d.comp_size[ci] + 1;
+    ++g_launches, lu_inverse_kernel<<<blocks_for(N), 128, 0, c.s>>>(d.lu.p + off[ci], d.perm.p + start[ci] + ci, N,
+                                                                   d.inv.p + ioff[ci], work.p);
+    CK_LAUNCH();
+    c.sync();
+  }
+  // the inverse kernel indexes per component through lu_off: store inverse
+  // offsets in place of the LU offsets for the throughput solve
+  d.inv_off.alloc(d.ncomp, c.s);
+  d.inv_off.upload(ioff.data(), d.ncomp);
+  c.sync();
+}
+
+void prepare_throughput(Ctx& c, DHier& h) {
+  for (size_t l = 0; l < h.levels.size(); ++l) {
+    DLevel& L = *h.levels[l];
+    const bool smooths = (L.coarsest == CM_RELAX) ||
+                         (L.coarsest == CM_NONE && l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_AGG);
+    if (smooths && !L.color) {
+      auto col = std::make_unique<DColor>();
+      build_coloring(c, L.op.view(), L.sched, *col);
+      // append the colour pointers after rp for the single-CTA kernel
+      DVec<int64_t> rp2(L.op.n + 1 + (col->ncolors + 2) / 2 + 1, c.s);
+      CK(cudaMemcpyAsync(rp2.p, col->rp.p, sizeof(int64_t) * (L.op.n + 1), cudaMemcpyDeviceToDevice, c.s));
+      CK(cudaMemcpyAsync(rp2.p + L.op.n + 1, col->cptr_h.data(), sizeof(int32_t) * (col->ncolors + 1),
+                         cudaMemcpyHostToDevice, c.s));
+      col->rp = std::move(rp2);
+      L.color = std::move(col);
+    }
+    if (L.direct) build_direct_inverse(c, *L.direct);
+  }
+  c.sync();
+}
+
+}  // namespace lamgb

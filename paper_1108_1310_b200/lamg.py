@@ -218,6 +218,7 @@ class LevelInfo:
     stage_used: int
     dummy_aggregate: int
     gs_fronts: int
+    colors: int = 0
 
 
 class Hierarchy:
@@ -249,7 +250,8 @@ class Hierarchy:
         li = _lib.lamg_level_info()
         _check(self.ctx.lib.lamg_hier_level_info(self.h, C.c_int32(l), C.byref(li)))
         return LevelInfo(li.kind, li.n, li.m, li.gamma, li.nu_pre, li.nu_post, li.tv_count, li.coarsest,
-                         li.nstages, li.coarse_n, li.alpha, li.stage_used, li.dummy_aggregate, li.gs_fronts)
+                         li.nstages, li.coarse_n, li.alpha, li.stage_used, li.dummy_aggregate, li.gs_fronts,
+                         li.colors)
 
     def op(self, l: int) -> SparseLaplacian:
         li = self.levels[l]
