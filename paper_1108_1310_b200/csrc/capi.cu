@@ -252,7 +252,9 @@ void lamg_hier_destroy(lamg_hier* h) {
     cudaSetDevice(h->h->device);
     cudaDeviceSynchronize();
   }
+  g_free_sync = true;
   delete h;
+  g_free_sync = false;
 }
 
 int lamg_hier_info(const lamg_hier* h, int32_t* nlevels, double* setup_work, int32_t* nwarnings,

@@ -9,6 +9,7 @@
 namespace lamgb {
 
 std::atomic<long long> g_launches{0};
+thread_local bool g_free_sync = false;
 
 void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   char buf[512];

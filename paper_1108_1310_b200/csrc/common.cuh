@@ -84,6 +84,10 @@ enum DevErrKind {
 };
 
 // ------------------------------------------------------------ device memory
+// When set (lamg_hier_destroy), buffers are freed synchronously: the stream
+// that allocated them may belong to a context destroyed in the meantime.
+extern thread_local bool g_free_sync;
+
 template <typename T>
 struct DVec {
   T* p = nullptr;
@@ -110,7 +114,10 @@ struct DVec {
     if (count > 0) CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, s));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      if (g_free_sync) cudaFree(p);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     n = 0;
   }

@@ -96,6 +96,11 @@ struct DHier {
   cudaStream_t owner_stream = nullptr;
   // throughput mode (colour-permuted copies), built on demand
   bool throughput_ready = false;
+  uint64_t uid = next_uid();  // workspaces key on this, not on the address
+  static uint64_t next_uid() {
+    static std::atomic<uint64_t> c{1};
+    return c++;
+  }
 };
 
 struct SetupOpts {

@@ -44,8 +44,8 @@ static void prof_mark(Ctx& c, int cls, bool begin, double bytes = 0.0) {
 
 // ------------------------------------------------------------- workspace
 void Workspace::ensure(Ctx& c, const DHier& h) {
-  if (owner == &h && lv.size() == h.levels.size()) return;
-  owner = &h;
+  if (owner == h.uid && lv.size() == h.levels.size()) return;
+  owner = h.uid;
   tail_built = false;
   lv.clear();
   lv.resize(h.levels.size());

@@ -44,7 +44,7 @@ struct LevelWS {
 
 // per-context solve workspace, sized for the last hierarchy solved
 struct Workspace {
-  const DHier* owner = nullptr;
+  uint64_t owner = 0;  // DHier::uid
   std::vector<LevelWS> lv;
   DVec<double> direct_scratch;
   bool top_rhs_valid = false;

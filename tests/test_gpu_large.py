@@ -1,0 +1,59 @@
+"""Size-independent parity at BASELINE.json scale (GPU).
+
+tests/golden/large.json holds SHA-256 digests of every hierarchy artefact and
+of the solution computed by the unmodified reference (make_golden_large.py).
+The GPU setup must reproduce every digest (bit-exact hierarchy), and the
+VALIDATE-mode solve must reproduce the cycle count, the residual history and
+the solution digest. The THROUGHPUT-mode solve (coloured smoother) must
+converge to the same tolerance with x within 1e-7 relative of the reference.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1108_1310_b200 import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "large.json")
+CASES = {
+    "cfg1_grid5_256": lambda: G.make_config(1),
+    "cfg2s_grid3d_64": lambda: G.grid3d_7pt(64),
+    "cfg3s_rgg_256k": lambda: G.rgg(1 << 18, seed=3),
+    "cfg4s_chunglu_256k": lambda: G.chung_lu(1 << 18, seed=4),
+    "cfg5s_rmat_16": lambda: G.rmat(16, seed=5),
+    "cfg2_grid3d_128": lambda: G.make_config(2),
+}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_large_config_matches_reference_digests(name):
+    from paper_1108_1310_b200 import lamg as L
+    g = json.load(open(GOLD))[name]
+    a = CASES[name]()
+    assert {k: sha(getattr(a, k)) for k in ("row_ptr", "col", "val", "diag")} == g["input_sha"]
+    b = G.gaussian_rhs(a.n, g["rhs_seed"])
+    x0 = G.default_x0(a.n)
+    assert sha(b) == g["b_sha"] and sha(x0) == g["x0_sha"]
+    ctx = L.Context(0, L.MODE_VALIDATE)
+    h = L.setup(a, ctx=ctx)
+    e = h.export()
+    got = {k: sha(v) for k, v in e.items()}
+    bad = [k for k, v in g["hier_sha"].items() if got.get(k) != v]
+    assert not bad, bad[:10]
+    x, st = L.solve(h, b, x0, ctx=ctx)
+    assert st.cycles == g["cycles"]
+    assert np.array_equal(np.array(st.residuals), np.array(g["residuals"]))
+    assert sha(x) == g["x_sha"]
+    ctx.set_mode(L.MODE_THROUGHPUT)
+    xt, stt = L.solve(h, b, x0, ctx=ctx)
+    assert stt.converged and stt.residuals[-1] <= stt.residuals[0] / 1e10
+    assert np.linalg.norm(xt - x) / np.linalg.norm(x) <= 1e-7
+    ctx.close()
