@@ -51,38 +51,7 @@ def peaks():
     return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-# ------------------------------------------------------------------ dist
-class Dist:
-    def __init__(self, want_gpu: bool):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-        if self.world > 1:
-            import torch
-            import torch.distributed as dist
-            backend = "nccl" if (want_gpu and torch.cuda.is_available()) else "gloo"
-            if backend == "nccl":
-                torch.cuda.set_device(self.local)
-            dist.init_process_group(backend=backend)
-            self.dist, self.backend = dist, backend
-
-    def barrier(self):
-        if self.world > 1:
-            self.dist.barrier()
-
-    def allreduce(self, v: float, op: str) -> float:
-        if self.world == 1:
-            return v
-        import torch
-        dev = "cuda" if self.backend == "nccl" else "cpu"
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
-        return float(t.item())
-
-    def close(self):
-        if self.world > 1:
-            self.dist.destroy_process_group()
+from paper_1108_1310_b200.dist import Dist  # noqa: E402
 
 
 # ---------------------------------------------------------------- clocks
