@@ -149,7 +149,7 @@ void gs_colored(Ctx& c, const DColor& col, int32_t n, const double* b, double* x
 void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, int group);
 inline int row_group_for(int64_t n, int64_t m) {
   const double deg = n ? 2.0 * (double)m / (double)n : 0.0;
-  return deg < 8.0 ? 1 : (deg < 24.0 ? 4 : 8);
+  return deg < 8.0 ? 1 : 8;
 }
 void build_direct_inverse(Ctx& c, DDirect& d);
 void prepare_throughput(Ctx& c, DHier& h);

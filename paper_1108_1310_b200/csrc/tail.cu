@@ -85,9 +85,12 @@ __device__ inline void gs_smem(const TLevel& L, const double* __restrict__ b, do
   const long long t1 = clock64();
   // G = 4 lanes per row, tree-folded (deterministic)
   constexpr int G = 4;
+  int32_t* s_cp = s_id + n;  // colour ranges (staged after the row ids)
+  for (int32_t i = threadIdx.x; i <= L.ncolors; i += blockDim.x) s_cp[i] = L.cptr[i];
+  __syncthreads();
   for (int sw = 0; sw < sweeps; ++sw)
     for (int32_t cc = 0; cc < L.ncolors; ++cc) {
-      const int32_t i0 = L.cptr[cc], i1 = L.cptr[cc + 1];
+      const int32_t i0 = s_cp[cc], i1 = s_cp[cc + 1];
       const int32_t span = ((i1 - i0) * G + 31) / 32 * 32;
       for (int32_t t = threadIdx.x; t < span; t += blockDim.x) {
         const int32_t i = i0 + t / G;
@@ -115,14 +118,82 @@ __device__ inline void gs_smem(const TLevel& L, const double* __restrict__ b, do
   }
 }
 
+// Coloured sweep with G lanes per row. The colour ranges are staged in shared
+// memory, and each group's first row of the NEXT phase (row id, extent,
+// diagonal, rhs and up to U entries per lane) is loaded before the barrier,
+// so the barrier wait hides those dependent loads; after it only the x
+// gathers and the fold remain on the critical path.
+constexpr int kMaxColors = 256;
+
 template <class S, int G>
-__device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, double* x, int sweeps) {
+__device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
+                                int32_t* s_cptr) {
+  constexpr int U = G == 1 ? 8 : 4;
+  const int nc = L.ncolors;
+  const bool cached = nc < kMaxColors;
+  if (cached) {
+    for (int i = threadIdx.x; i <= nc; i += blockDim.x) s_cptr[i] = L.cptr[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t slot = S::tid() / G;
+  bool p_ok = false;
+  int32_t p_u = 0;
+  int64_t p_k0 = 0, p_k1 = 0;
+  double p_d = 1.0, p_b = 0.0;
+  int32_t p_c[U];
+  double p_v[U];
+  auto prefetch = [&](int c) {
+    const int32_t c0 = cached ? s_cptr[c] : L.cptr[c];
+    const int32_t c1 = cached ? s_cptr[c + 1] : L.cptr[c + 1];
+    const int64_t i = c0 + slot;
+    p_ok = i < c1;
+    p_k0 = p_k1 = 0;
+    if (p_ok) {
+      p_u = L.row_ids[i];
+      p_k0 = L.prp[i];
+      p_k1 = L.prp[i + 1];
+      p_d = L.pdiag[i];
+      p_b = b[p_u];
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t k = p_k0 + lane + (int64_t)j * G;
+      const bool ok = k < p_k1;
+      p_c[j] = ok ? L.pcol[k] : 0;
+      p_v[j] = ok ? L.pval[k] : 0.0;
+    }
+  };
+  prefetch(0);
   for (int sw = 0; sw < sweeps; ++sw)
-    for (int32_t cc = 0; cc < L.ncolors; ++cc) {
-      const int32_t i0 = L.cptr[cc], i1 = L.cptr[cc + 1];
-      // whole warps iterate together (the group shuffles need every lane)
+    for (int32_t cc = 0; cc < nc; ++cc) {
+      const int32_t i0 = cached ? s_cptr[cc] : L.cptr[cc];
+      const int32_t i1 = cached ? s_cptr[cc + 1] : L.cptr[cc + 1];
+      {  // the prefetched row
+        double xv[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) xv[j] = (p_k0 + lane + (int64_t)j * G < p_k1) ? x[p_c[j]] : 0.0;
+        double acc;
+        if (G == 1) {
+          acc = p_b;
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (p_k0 + j < p_k1) acc = acc - p_v[j] * xv[j];
+          if (p_ok && p_k1 - p_k0 > U) acc = row_fold<8, true>(acc, L.pcol, L.pval, x, p_k0 + U, p_k1);
+          if (p_ok) x[p_u] = acc / p_d;
+        } else {
+          acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < U; ++j) acc += p_v[j] * xv[j];
+          for (int64_t k = p_k0 + lane + (int64_t)U * G; k < p_k1; k += G) acc += L.pval[k] * x[L.pcol[k]];
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+          if (p_ok && lane == 0) x[p_u] = (p_b - acc) / p_d;
+        }
+      }
+      // rows beyond the first slot of this colour (large levels only)
       const int64_t span = ((int64_t)(i1 - i0) * G + 31) / 32 * 32;
-      for (int64_t t = S::tid(); t < span; t += S::stride()) {
+      for (int64_t t = S::tid() + S::stride(); t < span; t += S::stride()) {
         const int64_t i = i0 + t / G;
         const bool ok = i < i1;
         if (G == 1) {
@@ -132,18 +203,21 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
           }
         } else {
           const double dot = group_dot<G>(L.pcol, L.pval, x, ok ? L.prp[i] : 0, ok ? L.prp[i + 1] : 0);
-          if (ok && (threadIdx.x & (G - 1)) == 0) {
+          if (ok && lane == 0) {
             const int32_t u = L.row_ids[i];
             x[u] = (b[u] - dot) / L.pdiag[i];
           }
         }
       }
+      const int next = cc + 1 < nc ? cc + 1 : (sw + 1 < sweeps ? 0 : -1);
+      if (next >= 0) prefetch(next);
       S::sync();
     }
 }
 
 template <class S>
 __device__ inline void gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps, TailCounters* ctr) {
+  __shared__ int32_t s_cptr[kMaxColors];
   if (L.ncolors == 0 || sweeps == 0) return;
   if (S::leader()) ctr->phases += (long long)sweeps * L.ncolors;
   if (!std::is_same<S, GridScope>::value && L.smem_ok) {
@@ -151,9 +225,9 @@ __device__ inline void gs(const TLevel& L, const double* __restrict__ b, double*
     return;
   }
   const long long tg = clock64();
-  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps);
-  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps);
-  else gs_group<S, 1>(L, b, x, sweeps);
+  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps, s_cptr);
+  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps, s_cptr);
+  else gs_group<S, 1>(L, b, x, sweeps, s_cptr);
   if (S::leader()) {
     ctr->cyc_global_gs += clock64() - tg;
     ctr->global_phases += (long long)sweeps * L.ncolors;
@@ -488,7 +562,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
       t.pcol = L.color->col.p;
       t.pval = L.color->val.p;
       t.pdiag = L.color->diag.p;
-      const int64_t bytes = (int64_t)a.n * (3 * 8 + 4 + 4) + 4 + 2 * a.m * 12;
+      const int64_t bytes = (int64_t)a.n * (3 * 8 + 4 + 4) + 4 + 2 * a.m * 12 + 4 * (L.color->ncolors + 1);
       t.smem_ok = bytes <= kTailSmem;
     }
     if (L.direct) {
