@@ -189,8 +189,6 @@ def run_lamg(args, dist: Dist):
     dev = dist.local
     torch.cuda.set_device(dev)
     S = args.streams
-    if "LAMG_TAIL_CTAS" not in os.environ:
-        os.environ["LAMG_TAIL_CTAS"] = str(max(8, min(64, 144 // S)))
     t0 = time.time()
     a, b, x0 = build_inputs(args.config, dist.rank)
     from paper_1108_1310_b200 import graphs as G
@@ -408,7 +406,7 @@ def main():
     ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-cycles", type=int, default=3)
-    ap.add_argument("--streams", type=int, default=8, help="concurrent right-hand sides per GPU")
+    ap.add_argument("--streams", type=int, default=16, help="concurrent right-hand sides per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")
     args = ap.parse_args()

@@ -9,6 +9,7 @@
 namespace lamgb {
 
 std::atomic<long long> g_launches{0};
+thread_local long long t_launches = 0;
 thread_local bool g_free_sync = false;
 
 void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
@@ -99,7 +100,7 @@ void Ctx::fetch_err_and_throw() {
 
 void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** args, size_t smem) {
   if (blocks < 1) blocks = 1;
-  ++g_launches;
+  count_launch();
   CK(cudaLaunchCooperativeKernel(kernel, dim3(blocks), dim3(threads), args, smem, c.s));
 }
 
@@ -244,11 +245,11 @@ __global__ void seq_fold_kernel(const double* __restrict__ x, int64_t n, double*
 }
 
 void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
-  ++g_launches, seq_fold_kernel<false><<<1, 32, 0, c.s>>>(x, n, d_out);
+  count_launch(), seq_fold_kernel<false><<<1, 32, 0, c.s>>>(x, n, d_out);
   CK_LAUNCH();
 }
 void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
-  ++g_launches, seq_fold_kernel<true><<<1, 32, 0, c.s>>>(x, n, d_out);
+  count_launch(), seq_fold_kernel<true><<<1, 32, 0, c.s>>>(x, n, d_out);
   CK_LAUNCH();
 }
 
@@ -286,15 +287,15 @@ __global__ void tree_final_kernel(const double* part, int np, double* out) {
 void tree_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
   double* part = c.dpart;
   int nb = (int)std::min<int64_t>(256, blocks_for(n));
-  ++g_launches, tree_partial_kernel<false><<<nb, kThreads, 0, c.s>>>(x, n, part);
-  ++g_launches, tree_final_kernel<false><<<1, 256, 0, c.s>>>(part, nb, d_out);
+  count_launch(), tree_partial_kernel<false><<<nb, kThreads, 0, c.s>>>(x, n, part);
+  count_launch(), tree_final_kernel<false><<<1, 256, 0, c.s>>>(part, nb, d_out);
   CK_LAUNCH();
 }
 void tree_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
   double* part = c.dpart;
   int nb = (int)std::min<int64_t>(256, blocks_for(n));
-  ++g_launches, tree_partial_kernel<true><<<nb, kThreads, 0, c.s>>>(x, n, part);
-  ++g_launches, tree_final_kernel<true><<<1, 256, 0, c.s>>>(part, nb, d_out);
+  count_launch(), tree_partial_kernel<true><<<nb, kThreads, 0, c.s>>>(x, n, part);
+  count_launch(), tree_final_kernel<true><<<1, 256, 0, c.s>>>(part, nb, d_out);
   CK_LAUNCH();
 }
 

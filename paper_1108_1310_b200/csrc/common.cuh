@@ -25,6 +25,11 @@ namespace cg = cooperative_groups;
 
 // kernels launched by this library (all contexts); lamg_launch_count()
 extern std::atomic<long long> g_launches;
+extern thread_local long long t_launches;  // this thread's share (graph capture accounting)
+inline void count_launch() {
+  ++g_launches;
+  ++t_launches;
+}
 
 // ----------------------------------------------------------------- errors
 struct LamgError : std::runtime_error {

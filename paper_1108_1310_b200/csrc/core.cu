@@ -22,7 +22,7 @@ __global__ void residual_exact_kernel(CSRv a, const double* __restrict__ b,
 
 void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r) {
   if (a.n == 0) return;
-  ++g_launches, residual_exact_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, b, x, r);
+  count_launch(), residual_exact_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, b, x, r);
   CK_LAUNCH();
 }
 
@@ -90,8 +90,8 @@ void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
   if (n == 0) return;
   DVec<int32_t> cnt(n, c.s), level(n, c.s), queue(n, c.s);
   DVec<uint8_t> flag(n, c.s);
-  ++g_launches, deps_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, backward, cnt.p);
-  ++g_launches, zero_dep_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(cnt.p, n, flag.p);
+  count_launch(), deps_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, backward, cnt.p);
+  count_launch(), zero_dep_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(cnt.p, n, flag.p);
   CK_LAUNCH();
   int32_t first = (int32_t)select_flagged_index(c, flag.p, queue.p, n);
   int32_t* ctl = c.dflag + 8;
@@ -108,14 +108,14 @@ void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
   // rows sorted by (front, row): stable radix sort of the identity by front
   DVec<uint32_t> keys_out(n, c.s);
   DVec<int32_t> ids(n, c.s);
-  ++g_launches, iota_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
+  count_launch(), iota_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
   CK_LAUNCH();
   out.rows.alloc(n, c.s);
   int bits = 1;
   while ((1u << bits) <= (uint32_t)nf && bits < 32) ++bits;
   sort_pairs_u32_i32(c, (const uint32_t*)level.p, keys_out.p, ids.p, out.rows.p, n, bits);
   out.front_ptr.alloc(nf + 1, c.s);
-  ++g_launches, front_bounds_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(keys_out.p, n, out.front_ptr.p, nf);
+  count_launch(), front_bounds_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(keys_out.p, n, out.front_ptr.p, nf);
   CK_LAUNCH();
   out.nfronts = nf;
   std::vector<int32_t> fp = out.front_ptr.to_host();
@@ -200,10 +200,10 @@ void build_upper_index(Ctx& c, const CSRv& a, UpperIndex& out) {
   if (nnz == 0) return;
   DVec<uint8_t> flag(nnz, c.s);
   DVec<int32_t> row_of(nnz, c.s);
-  ++g_launches, upper_flags_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, flag.p, row_of.p);
+  count_launch(), upper_flags_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, flag.p, row_of.p);
   CK_LAUNCH();
   out.count = select_flagged_index64(c, flag.p, out.entry.p, nnz);
-  ++g_launches, gather_rows_kernel<<<blocks_for(out.count), kThreads, 0, c.s>>>(out.entry.p, row_of.p, out.count, out.row.p);
+  count_launch(), gather_rows_kernel<<<blocks_for(out.count), kThreads, 0, c.s>>>(out.entry.p, row_of.p, out.count, out.row.p);
   CK_LAUNCH();
 }
 
@@ -223,7 +223,7 @@ void energy_seq(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, do
     CK(cudaMemsetAsync(d_out, 0, sizeof(double), c.s));
     return;
   }
-  ++g_launches, energy_terms_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, x, scratch.p);
+  count_launch(), energy_terms_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, x, scratch.p);
   CK_LAUNCH();
   seq_sum(c, scratch.p, up.count, d_out);
 }
@@ -244,7 +244,7 @@ __global__ void fill_pm1_kernel(double* x, int64_t n, uint64_t s0, int stride, i
 void fill_pm1(Ctx& c, double* x, int64_t n, uint64_t seed, int stride, int offset) {
   if (n == 0) return;
   uint64_t s0 = seed ? seed : 0x9e3779b97f4a7c15ULL;
-  ++g_launches, fill_pm1_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, s0, stride, offset);
+  count_launch(), fill_pm1_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, s0, stride, offset);
   CK_LAUNCH();
 }
 
@@ -270,10 +270,10 @@ void subtract_mean_seq(Ctx& c, double* x, int64_t n, int K) {
   double* sums = c.dscal + 64;  // [64..80)
   if (K == 1) seq_sum(c, x, n, sums);
   else {
-    ++g_launches, col_seq_sum_kernel<<<1, 32, 0, c.s>>>(x, n, K, sums);
+    count_launch(), col_seq_sum_kernel<<<1, 32, 0, c.s>>>(x, n, K, sums);
     CK_LAUNCH();
   }
-  ++g_launches, sub_mean_kernel<<<blocks_for(n * K), kThreads, 0, c.s>>>(x, n, K, sums);
+  count_launch(), sub_mean_kernel<<<blocks_for(n * K), kThreads, 0, c.s>>>(x, n, K, sums);
   CK_LAUNCH();
 }
 
@@ -281,7 +281,7 @@ void subtract_mean_tree(Ctx& c, double* x, int64_t n) {
   if (n == 0) return;
   double* sums = c.dscal + 64;
   tree_sum(c, x, n, sums);
-  ++g_launches, sub_mean_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, 1, sums);
+  count_launch(), sub_mean_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(x, n, 1, sums);
   CK_LAUNCH();
 }
 
@@ -335,10 +335,10 @@ void validate_exact(Ctx& c, const CSRv& a) {
   if (a.n <= 0) throw LamgError(LAMG_E_INVALID_LAPLACIAN, "empty matrix");
   unsigned long long* md = (unsigned long long*)(c.dscal + 90);
   CK(cudaMemsetAsync(md, 0, sizeof(unsigned long long), c.s));
-  ++g_launches, abs_max_kernel<<<std::min(blocks_for(a.n), 1024), kThreads, 0, c.s>>>(a.diag, a.n, md);
+  count_launch(), abs_max_kernel<<<std::min(blocks_for(a.n), 1024), kThreads, 0, c.s>>>(a.diag, a.n, md);
   CK_LAUNCH();
   c.checked([&] {
-    ++g_launches, validate_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, md, c.derr);
+    count_launch(), validate_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, md, c.derr);
     CK_LAUNCH();
   });
 }
@@ -356,7 +356,7 @@ __global__ void restrict_kernel(int32_t cn, const int64_t* __restrict__ mem_ptr,
 void restrict_exact(Ctx& c, int32_t coarse_n, const int64_t* mem_ptr, const int32_t* mem,
                     const double* r, double mu, double* rc) {
   if (coarse_n == 0) return;
-  ++g_launches, restrict_kernel<<<blocks_for(coarse_n), kThreads, 0, c.s>>>(coarse_n, mem_ptr, mem, r, mu, rc);
+  count_launch(), restrict_kernel<<<blocks_for(coarse_n), kThreads, 0, c.s>>>(coarse_n, mem_ptr, mem, r, mu, rc);
   CK_LAUNCH();
 }
 
@@ -367,7 +367,7 @@ __global__ void interpolate_kernel(int32_t n, const int32_t* __restrict__ agg,
 }
 void interpolate(Ctx& c, int32_t fine_n, const int32_t* agg, const double* ec, double* x) {
   if (fine_n == 0) return;
-  ++g_launches, interpolate_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(fine_n, agg, ec, x);
+  count_launch(), interpolate_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(fine_n, agg, ec, x);
   CK_LAUNCH();
 }
 
@@ -385,7 +385,7 @@ __global__ void coarsen_rhs_kernel(StageV s, const double* __restrict__ b, doubl
 }
 void coarsen_rhs(Ctx& c, const StageV& s, const double* b, double* bc) {
   if (s.coarse_n == 0) return;
-  ++g_launches, coarsen_rhs_kernel<<<blocks_for(s.coarse_n), kThreads, 0, c.s>>>(s, b, bc);
+  count_launch(), coarsen_rhs_kernel<<<blocks_for(s.coarse_n), kThreads, 0, c.s>>>(s, b, bc);
   CK_LAUNCH();
 }
 
@@ -399,12 +399,12 @@ __global__ void scatter_kernel(double* dst, const double* src, const int32_t* id
 }
 void gather_d(Ctx& c, double* dst, const double* src, const int32_t* idx, int64_t n) {
   if (n == 0) return;
-  ++g_launches, gather_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
+  count_launch(), gather_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
   CK_LAUNCH();
 }
 void scatter_d(Ctx& c, double* dst, const double* src, const int32_t* idx, int64_t n) {
   if (n == 0) return;
-  ++g_launches, scatter_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
+  count_launch(), scatter_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(dst, src, idx, n);
   CK_LAUNCH();
 }
 void copy_d(Ctx& c, double* dst, const double* src, int64_t n) {
@@ -424,7 +424,7 @@ __global__ void backsub_f_kernel(StageV s, const double* __restrict__ b, double*
 void backsub(Ctx& c, const StageV& s, const double* xc, const double* b, double* x) {
   scatter_d(c, x, xc, s.poc, s.coarse_n);
   if (s.nf == 0) return;
-  ++g_launches, backsub_f_kernel<<<blocks_for(s.nf), kThreads, 0, c.s>>>(s, b, x);
+  count_launch(), backsub_f_kernel<<<blocks_for(s.nf), kThreads, 0, c.s>>>(s, b, x);
   CK_LAUNCH();
 }
 
@@ -466,18 +466,18 @@ void build_stage_transpose(Ctx& c, int32_t coarse_n, int32_t nf, const int64_t* 
   }
   DVec<uint32_t> key(nnzf, c.s);
   DVec<int64_t> ids(nnzf, c.s);
-  ++g_launches, stage_keys_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(nf, f_ptr, f_nbr, cop, key.p, f_of_p.p);
-  ++g_launches, iota64_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(ids.p, nnzf);
+  count_launch(), stage_keys_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(nf, f_ptr, f_nbr, cop, key.p, f_of_p.p);
+  count_launch(), iota64_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(ids.p, nnzf);
   CK_LAUNCH();
   // stable sort of contribution indices p by target coarse node: within a
   // target, p ascending == (f asc, p asc), the reference's accumulation order
   int bits = 1;
   while ((1ull << bits) <= (unsigned long long)coarse_n && bits < 32) ++bits;
   DVec<uint64_t> k64(nnzf, c.s), k64s(nnzf, c.s);
-  ++g_launches, widen_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(key.p, nnzf, k64.p);
+  count_launch(), widen_kernel<<<blocks_for(nnzf), kThreads, 0, c.s>>>(key.p, nnzf, k64.p);
   CK_LAUNCH();
   sort_pairs_u64(c, k64.p, k64s.p, ids.p, t_p.p, nnzf, bits);
-  ++g_launches, seg_bounds64_kernel<<<blocks_for(nnzf + 1), kThreads, 0, c.s>>>(k64s.p, nnzf, coarse_n, t_ptr.p);
+  count_launch(), seg_bounds64_kernel<<<blocks_for(nnzf + 1), kThreads, 0, c.s>>>(k64s.p, nnzf, coarse_n, t_ptr.p);
   CK_LAUNCH();
 }
 
@@ -493,12 +493,12 @@ void build_members(Ctx& c, int32_t fine_n, int32_t coarse_n, const int32_t* agg,
   mem.alloc(fine_n, c.s);
   DVec<uint64_t> key(fine_n, c.s), key_sorted(fine_n, c.s);
   DVec<int32_t> ids(fine_n, c.s);
-  ++g_launches, agg_keys_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(agg, fine_n, key.p, ids.p);
+  count_launch(), agg_keys_kernel<<<blocks_for(fine_n), kThreads, 0, c.s>>>(agg, fine_n, key.p, ids.p);
   CK_LAUNCH();
   int bits = 1;
   while ((1ull << bits) <= (unsigned long long)coarse_n && bits < 32) ++bits;
   sort_pairs_u64_i32(c, key.p, key_sorted.p, ids.p, mem.p, fine_n, bits);
-  ++g_launches, seg_bounds64_kernel<<<blocks_for(fine_n + 1), kThreads, 0, c.s>>>(key_sorted.p, fine_n, coarse_n, mem_ptr.p);
+  count_launch(), seg_bounds64_kernel<<<blocks_for(fine_n + 1), kThreads, 0, c.s>>>(key_sorted.p, fine_n, coarse_n, mem_ptr.p);
   CK_LAUNCH();
 }
 

@@ -104,25 +104,25 @@ static void assemble_canonical_dev(Ctx& c, int32_t n, int64_t E, const int32_t* 
   DVec<int32_t> vperm(std::max<int64_t>(E, 1), c.s);
   if (E > 0) {
     // u-segments: eu is sorted
-    ++g_launches, seg_bounds_i32_kernel<<<blocks_for(E + 1), kThreads, 0, c.s>>>(eu, E, n, uptr.p);
+    count_launch(), seg_bounds_i32_kernel<<<blocks_for(E + 1), kThreads, 0, c.s>>>(eu, E, n, uptr.p);
     // v-segments: stable sort of edge ids by v
     DVec<uint64_t> k(E, c.s), ks(E, c.s);
     DVec<int32_t> ids(E, c.s), vs(E, c.s);
-    ++g_launches, ev_keys_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ev, E, k.p, ids.p);
+    count_launch(), ev_keys_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ev, E, k.p, ids.p);
     CK_LAUNCH();
     sort_pairs_u64_i32(c, k.p, ks.p, ids.p, vperm.p, E, bits_for((uint64_t)n));
-    ++g_launches, narrow_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ks.p, E, vs.p);
-    ++g_launches, seg_bounds_i32_kernel<<<blocks_for(E + 1), kThreads, 0, c.s>>>(vs.p, E, n, vptr.p);
+    count_launch(), narrow_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ks.p, E, vs.p);
+    count_launch(), seg_bounds_i32_kernel<<<blocks_for(E + 1), kThreads, 0, c.s>>>(vs.p, E, n, vptr.p);
     CK_LAUNCH();
   } else {
     uptr.zero();
     vptr.zero();
   }
-  ++g_launches, row_counts_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, uptr.p, vptr.p, cnt.p);
+  count_launch(), row_counts_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, uptr.p, vptr.p, cnt.p);
   CK_LAUNCH();
   CK(cudaMemsetAsync(cnt.p + n, 0, sizeof(int64_t), c.s));
   exclusive_scan_i64(c, cnt.p, out.rp.p, n + 1);
-  ++g_launches, assemble_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, E, eu, ev, ew, uptr.p, vptr.p, vperm.p,
+  count_launch(), assemble_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, E, eu, ev, ew, uptr.p, vptr.p, vperm.p,
                                                           out.rp.p, out.col.p, out.val.p, out.diag.p);
   CK_LAUNCH();
 }
@@ -169,19 +169,19 @@ static void fold_contribs_and_assemble(Ctx& c, int32_t coarse_n, int64_t nc, DVe
   keys.release();
   w.release();
   DVec<uint8_t> head(nc, c.s);
-  ++g_launches, seg_heads_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(ks.p, nc, head.p);
+  count_launch(), seg_heads_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(ks.p, nc, head.p);
   CK_LAUNCH();
   DVec<int64_t> heads(nc, c.s);
   int64_t nseg = select_flagged_index64(c, head.p, heads.p, nc);
   DVec<double> sum(nseg, c.s);
   DVec<uint8_t> keep(nseg, c.s);
-  ++g_launches, seg_fold_kernel<<<blocks_for(nseg), kThreads, 0, c.s>>>(ks.p, ws.p, heads.p, nseg, nc, sum.p, keep.p);
+  count_launch(), seg_fold_kernel<<<blocks_for(nseg), kThreads, 0, c.s>>>(ks.p, ws.p, heads.p, nseg, nc, sum.p, keep.p);
   CK_LAUNCH();
   DVec<int64_t> kidx(nseg, c.s);
   int64_t ne = select_flagged_index64(c, keep.p, kidx.p, nseg);
   DVec<int32_t> eu(std::max<int64_t>(ne, 1), c.s), ev(std::max<int64_t>(ne, 1), c.s);
   DVec<double> ew(std::max<int64_t>(ne, 1), c.s);
-  ++g_launches, emit_edges_kernel<<<blocks_for(ne), kThreads, 0, c.s>>>(kidx.p, ne, heads.p, ks.p, sum.p, eu.p, ev.p, ew.p);
+  count_launch(), emit_edges_kernel<<<blocks_for(ne), kThreads, 0, c.s>>>(kidx.p, ne, heads.p, ks.p, sum.p, eu.p, ev.p, ew.p);
   CK_LAUNCH();
   assemble_canonical_dev(c, coarse_n, ne, eu.p, ev.p, ew.p, out);
 }
@@ -219,13 +219,13 @@ void galerkin(Ctx& c, const CSRv& a, const int32_t* agg, int32_t coarse_n, DCSR&
   UpperIndex up;
   build_upper_index(c, a, up);
   DVec<uint8_t> flag(std::max<int64_t>(up.count, 1), c.s);
-  ++g_launches, galerkin_flags_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, agg, flag.p);
+  count_launch(), galerkin_flags_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, agg, flag.p);
   CK_LAUNCH();
   DVec<int64_t> sel(std::max<int64_t>(up.count, 1), c.s);
   int64_t nc = select_flagged_index64(c, flag.p, sel.p, up.count);
   DVec<uint64_t> keys(std::max<int64_t>(nc, 1), c.s);
   DVec<double> w(std::max<int64_t>(nc, 1), c.s);
-  ++g_launches, galerkin_emit_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, sel.p, nc, agg, keys.p, w.p);
+  count_launch(), galerkin_emit_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, sel.p, nc, agg, keys.p, w.p);
   CK_LAUNCH();
   fold_contribs_and_assemble(c, coarse_n, nc, keys, w, out);
   c.work += (double)a.m;
@@ -294,7 +294,7 @@ void select_low_degree(Ctx& c, const CSRv& a, int32_t max_degree, SelectResult& 
   DVec<int8_t> state(n, c.s);
   int32_t* undecided = c.dflag + 16;
   CK(cudaMemsetAsync(undecided, 0, sizeof(int32_t), c.s));
-  ++g_launches, mis_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, max_degree, state.p, undecided);
+  count_launch(), mis_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, max_degree, state.p, undecided);
   CK_LAUNCH();
   const int threads = 256;
   int blocks = std::min(c.max_coop_blocks((const void*)mis_rounds_kernel, threads), blocks_for(n, threads));
@@ -303,7 +303,7 @@ void select_low_degree(Ctx& c, const CSRv& a, int32_t max_degree, SelectResult& 
   void* args[] = {&av, &state.p, &undecided};
   coop_launch(c, (const void*)mis_rounds_kernel, blocks, threads, args);
   DVec<uint8_t> ff(n, c.s), cf(n, c.s);
-  ++g_launches, mis_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(state.p, n, ff.p, cf.p);
+  count_launch(), mis_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(state.p, n, ff.p, cf.p);
   CK_LAUNCH();
   out.f.alloc(n, c.s);
   out.c.alloc(n, c.s);
@@ -405,8 +405,8 @@ void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int
   st.coarse_n = nc;
   st.nf = nf;
   st.cop.alloc(n, c.s);
-  ++g_launches, cop_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, st.cop.p);
-  ++g_launches, cop_set_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(cset, nc, st.cop.p);
+  count_launch(), cop_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, st.cop.p);
+  count_launch(), cop_set_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(cset, nc, st.cop.p);
   CK_LAUNCH();
   st.poc.alloc(std::max(nc, 1), c.s);
   if (nc) CK(cudaMemcpyAsync(st.poc.p, cset, sizeof(int32_t) * nc, cudaMemcpyDeviceToDevice, c.s));
@@ -415,14 +415,14 @@ void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int
   if (check_inputs && nf) {
     CSRv av = a;
     c.checked([&] {
-      ++g_launches, schur_check_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(av, f, nf, st.cop.p, c.derr);
+      count_launch(), schur_check_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(av, f, nf, st.cop.p, c.derr);
       CK_LAUNCH();
     });
   }
   DVec<int64_t> deg(nf + 1, c.s), pairs(nf + 1, c.s), poff(nf + 1, c.s);
   st.f_ptr.alloc(nf + 1, c.s);
   if (nf) {
-    ++g_launches, f_deg_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(a, f, nf, deg.p, pairs.p);
+    count_launch(), f_deg_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(a, f, nf, deg.p, pairs.p);
     CK_LAUNCH();
   }
   CK(cudaMemsetAsync(deg.p + nf, 0, sizeof(int64_t), c.s));
@@ -435,13 +435,13 @@ void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int
   st.f_nbr.alloc(std::max<int64_t>(st.nnzf, 1), c.s);
   st.f_val.alloc(std::max<int64_t>(st.nnzf, 1), c.s);
   if (nf) {
-    ++g_launches, stage_fill_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(a, f, nf, st.f_ptr.p, st.f_diag.p, st.f_nbr.p, st.f_val.p);
+    count_launch(), stage_fill_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(a, f, nf, st.f_ptr.p, st.f_diag.p, st.f_nbr.p, st.f_val.p);
     CK_LAUNCH();
   }
   // emission: C-C edges first, then the fill cliques
   DVec<int64_t> ccnt(nc + 1, c.s), coff(nc + 1, c.s);
   if (nc) {
-    ++g_launches, cc_count_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, cset, nc, st.cop.p, ccnt.p);
+    count_launch(), cc_count_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, cset, nc, st.cop.p, ccnt.p);
     CK_LAUNCH();
   }
   CK(cudaMemsetAsync(ccnt.p + nc, 0, sizeof(int64_t), c.s));
@@ -450,9 +450,9 @@ void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int
   int64_t total = ncc + npairs;
   DVec<uint64_t> keys(std::max<int64_t>(total, 1), c.s);
   DVec<double> w(std::max<int64_t>(total, 1), c.s);
-  if (nc) ++g_launches, cc_emit_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, cset, nc, st.cop.p, coff.p, keys.p, w.p);
+  if (nc) count_launch(), cc_emit_kernel<<<blocks_for(nc), kThreads, 0, c.s>>>(a, cset, nc, st.cop.p, coff.p, keys.p, w.p);
   if (nf)
-    ++g_launches, fill_emit_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(nf, st.f_ptr.p, st.f_nbr.p, st.f_val.p, st.f_diag.p,
+    count_launch(), fill_emit_kernel<<<blocks_for(nf), kThreads, 0, c.s>>>(nf, st.f_ptr.p, st.f_nbr.p, st.f_val.p, st.f_diag.p,
                                                            st.cop.p, poff.p, ncc, keys.p, w.p);
   CK_LAUNCH();
   fold_contribs_and_assemble(c, nc, total, keys, w, coarse);
@@ -559,8 +559,8 @@ __global__ void affinity_kernel(CSRv a, const double* __restrict__ X, int K,
 }
 
 void compute_affinities(Ctx& c, const CSRv& a, int K, const double* X, double* aff, double* nn) {
-  ++g_launches, node_norm_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(X, a.n, K, nn);
-  ++g_launches, affinity_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, X, K, nn, aff);
+  count_launch(), node_norm_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(X, a.n, K, nn);
+  count_launch(), affinity_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, X, K, nn, aff);
   CK_LAUNCH();
   c.work += (double)K * (double)a.m;
 }
@@ -584,7 +584,7 @@ __global__ void hub_flags_kernel(CSRv a, uint8_t* flag) {
 
 int32_t detect_hubs(Ctx& c, const CSRv& a, DVec<int32_t>& hubs) {
   DVec<uint8_t> flag(a.n, c.s);
-  ++g_launches, hub_flags_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, flag.p);
+  count_launch(), hub_flags_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, flag.p);
   CK_LAUNCH();
   hubs.alloc(a.n, c.s);
   return (int32_t)select_flagged_index(c, flag.p, hubs.p, a.n);
@@ -803,34 +803,34 @@ void aggregate(Ctx& c, const CSRv& a, int K, const double* X, double gamma, cons
   const int64_t nnz = 2 * a.m;
   DVec<double> aff(std::max<int64_t>(nnz, 1), c.s), nn(n, c.s), strongest(n, c.s);
   compute_affinities(c, a, K, X, aff.p, nn.p);
-  ++g_launches, strongest_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p);
+  count_launch(), strongest_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p);
   DVec<uint8_t> dummy(n, c.s);
-  ++g_launches, dummy_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p, dummy.p);
+  count_launch(), dummy_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p, dummy.p);
   DVec<int8_t> status(n, c.s), done(n, c.s);
   DVec<int32_t> seed_ref(n, c.s);
-  ++g_launches, status_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, status.p, seed_ref.p);
-  if (nhubs) ++g_launches, hubs_seed_kernel<<<blocks_for(nhubs), kThreads, 0, c.s>>>(hubs, nhubs, dummy.p, status.p);
+  count_launch(), status_init_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, status.p, seed_ref.p);
+  if (nhubs) count_launch(), hubs_seed_kernel<<<blocks_for(nhubs), kThreads, 0, c.s>>>(hubs, nhubs, dummy.p, status.p);
   CK_LAUNCH();
   // stage-1 visiting order: (min affinity, node) ascending
   DVec<uint8_t> inorder(n, c.s);
   DVec<uint64_t> key(n, c.s);
-  ++g_launches, order_key_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p, dummy.p, status.p, aff.p, inorder.p, key.p);
+  count_launch(), order_key_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, strongest.p, dummy.p, status.p, aff.p, inorder.p, key.p);
   CK_LAUNCH();
   DVec<int32_t> members(n, c.s);
   int32_t norder = (int32_t)select_flagged_index(c, inorder.p, members.p, n);
   DVec<int32_t> order(std::max(norder, 1), c.s), pos(n, c.s);
-  ++g_launches, fill_i32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(pos.p, n, -1);
+  count_launch(), fill_i32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(pos.p, n, -1);
   CK_LAUNCH();
   if (norder) {
     DVec<uint64_t> k1(norder, c.s), k2(norder, c.s);
-    ++g_launches, gather_keys_kernel<<<blocks_for(norder), kThreads, 0, c.s>>>(members.p, norder, key.p, k1.p);
+    count_launch(), gather_keys_kernel<<<blocks_for(norder), kThreads, 0, c.s>>>(members.p, norder, key.p, k1.p);
     CK_LAUNCH();
     sort_pairs_u64_i32(c, k1.p, k2.p, members.p, order.p, norder, 64);  // stable: ties by node
-    ++g_launches, order_pos_kernel<<<blocks_for(norder), kThreads, 0, c.s>>>(order.p, norder, pos.p);
+    count_launch(), order_pos_kernel<<<blocks_for(norder), kThreads, 0, c.s>>>(order.p, norder, pos.p);
     CK_LAUNCH();
   }
   DVec<uint8_t> cand(std::max<int64_t>(nnz, 1), c.s);
-  ++g_launches, candidate_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, X, K, strongest.p, dummy.p, cand.p);
+  count_launch(), candidate_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, X, K, strongest.p, dummy.p, cand.p);
   CK_LAUNCH();
   done.zero();
   int32_t* remaining = c.dflag + 20;
@@ -848,9 +848,9 @@ void aggregate(Ctx& c, const CSRv& a, int K, const double* X, double gamma, cons
   int32_t* nonassoc = c.dflag + 25;
   int32_t init[2] = {std::numeric_limits<int32_t>::max(), 0};
   CK(cudaMemcpyAsync(first_dummy, init, sizeof init, cudaMemcpyHostToDevice, c.s));
-  ++g_launches, first_dummy_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, first_dummy);
+  count_launch(), first_dummy_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, first_dummy);
   DVec<int32_t> root(n + 1, c.s), ids(n + 1, c.s);
-  ++g_launches, root_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, first_dummy, root.p, nonassoc);
+  count_launch(), root_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, first_dummy, root.p, nonassoc);
   CK_LAUNCH();
   CK(cudaMemsetAsync(root.p + n, 0, sizeof(int32_t), c.s));
   exclusive_scan_i32(c, root.p, ids.p, n + 1);
@@ -863,9 +863,9 @@ void aggregate(Ctx& c, const CSRv& a, int K, const double* X, double gamma, cons
   out.coarse_n = coarse_n;
   out.aggregate_of.alloc(n, c.s);
   out.seed_of.alloc(std::max(coarse_n, 1), c.s);
-  ++g_launches, number_roots_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, root.p, ids.p, first_dummy,
+  count_launch(), number_roots_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, root.p, ids.p, first_dummy,
                                                          out.aggregate_of.p, out.seed_of.p);
-  ++g_launches, number_assoc_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, seed_ref.p, out.aggregate_of.p);
+  count_launch(), number_assoc_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, dummy.p, status.p, seed_ref.p, out.aggregate_of.p);
   CK_LAUNCH();
   if (has_dummy) out.dummy_aggregate = read_i32(c, ids.p + hv[0]);
   else out.dummy_aggregate = -1;
@@ -1004,7 +1004,7 @@ void make_direct(Ctx& c, const CSRv& a, DDirect& d) {
   d.n = n;
   d.m = a.m;
   DVec<int32_t> label(n, c.s);
-  ++g_launches, labels_kernel<<<1, 1024, 0, c.s>>>(a, label.p);
+  count_launch(), labels_kernel<<<1, 1024, 0, c.s>>>(a, label.p);
   CK_LAUNCH();
   std::vector<int32_t> lab = label.to_host();
   // components in order of their smallest node, nodes ascending (BFS order of
@@ -1048,12 +1048,12 @@ void make_direct(Ctx& c, const CSRv& a, DDirect& d) {
     const bool whole = d.ncomp == 1;
     const int32_t* nodes = d.nodes.p + hstart[ci];
     if (!whole) {
-      ++g_launches, local_index_kernel<<<blocks_for(cn), kThreads, 0, c.s>>>(nodes, cn, local.p);
+      count_launch(), local_index_kernel<<<blocks_for(cn), kThreads, 0, c.s>>>(nodes, cn, local.p);
       CK_LAUNCH();
     }
     double* M = d.lu.p + hoff[ci];
-    ++g_launches, bordered_kernel<<<1, 1024, 0, c.s>>>(a, nodes, cn, whole, local.p, M);
-    ++g_launches, lu_kernel<<<1, 1024, 0, c.s>>>(M, cn + 1, d.perm.p + hstart[ci] + ci);
+    count_launch(), bordered_kernel<<<1, 1024, 0, c.s>>>(a, nodes, cn, whole, local.p, M);
+    count_launch(), lu_kernel<<<1, 1024, 0, c.s>>>(M, cn + 1, d.perm.p + hstart[ci] + ci);
     CK_LAUNCH();
   }
   const double nn1 = (double)n + 1.0;
@@ -1119,10 +1119,10 @@ __global__ void direct_inv_kernel(const int32_t* comp_start, int32_t ncomp, cons
 
 void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exact, double* scratch) {
   if (exact || d.inv.n == 0) {
-    ++g_launches, direct_solve_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.lu_off.p, d.lu.p, d.perm.p,
+    count_launch(), direct_solve_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.lu_off.p, d.lu.p, d.perm.p,
                                             d.ncomp == 1, b, x, scratch, scratch + d.maxN + 1);
   } else {
-    ++g_launches, direct_inv_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.inv_off.p, d.inv.p,
+    count_launch(), direct_inv_kernel<<<1, 256, 0, c.s>>>(d.comp_start.p, d.ncomp, d.nodes.p, d.inv_off.p, d.inv.p,
                                           d.ncomp == 1, b, x);
   }
   CK_LAUNCH();

@@ -43,10 +43,17 @@ static void prof_mark(Ctx& c, int cls, bool begin, double bytes = 0.0) {
 }
 
 // ------------------------------------------------------------- workspace
+void Workspace::clear_graphs() {
+  for (auto& g : graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs.clear();
+}
+
 void Workspace::ensure(Ctx& c, const DHier& h) {
   if (owner == h.uid && lv.size() == h.levels.size()) return;
   owner = h.uid;
   tail_built = false;
+  clear_graphs();
   lv.clear();
   lv.resize(h.levels.size());
   int32_t maxN = 0;
@@ -54,10 +61,8 @@ void Workspace::ensure(Ctx& c, const DHier& h) {
     const DLevel& L = *h.levels[l];
     LevelWS& w = lv[l];
     const int32_t n = L.op.n;
-    if (l > 0) {
-      w.b.alloc(n, c.s);
-      w.x.alloc(n, c.s);
-    }
+    w.b.alloc(n, c.s);  // level 0: fixed-address copies of the solve's b and x (graph replay)
+    w.x.alloc(n, c.s);
     w.r.alloc(n, c.s);
     if (L.direct) maxN = std::max(maxN, L.direct->maxN);
     if (l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_ELIM) {
@@ -176,30 +181,30 @@ static void recombine(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS&
   c.work += (double)a.m;
   double* dots = c.dscal + 120;  // [120..126]
   CK(cudaMemsetAsync(dots, 0, 7 * sizeof(double), c.s));
-  ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.r.p, w.tmp.p, n);
+  count_launch(), prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.r.p, w.tmp.p, n);
   fold_sum(c, exact, w.tmp.p, n, dots + 0);
   DVec<double> ad[2];
   for (int i = 0; i < cols; ++i) {
     ad[i].alloc(n, c.s);
-    ++g_launches, diff_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.saved_r[i].p, ad[i].p, n);
+    count_launch(), diff_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, w.saved_r[i].p, ad[i].p, n);
   }
   for (int i = 0; i < cols; ++i) {
-    ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, ad[i].p, w.tmp.p, n);
+    count_launch(), prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(w.r.p, ad[i].p, w.tmp.p, n);
     fold_sum(c, exact, w.tmp.p, n, dots + 1 + i);
     for (int j = 0; j <= i; ++j) {
-      ++g_launches, prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ad[i].p, ad[j].p, w.tmp.p, n);
+      count_launch(), prod_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ad[i].p, ad[j].p, w.tmp.p, n);
       int slot = (i == 0 && j == 0) ? 3 : (i == 1 && j == 0) ? 4 : 5;
       fold_sum(c, exact, w.tmp.p, n, dots + slot);
     }
   }
   double* alpha = c.dscal + 130;
-  ++g_launches, recomb_alpha_kernel<<<1, 1, 0, c.s>>>(dots, cols, alpha);
-  ++g_launches, recomb_update_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, cols, alpha, w.r.p, w.saved_r[0].p,
+  count_launch(), recomb_alpha_kernel<<<1, 1, 0, c.s>>>(dots, cols, alpha);
+  count_launch(), recomb_update_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(n, cols, alpha, w.r.p, w.saved_r[0].p,
                                                             cols > 1 ? w.saved_r[1].p : w.saved_r[0].p,
                                                             w.saved_x[0].p, cols > 1 ? w.saved_x[1].p : w.saved_x[0].p,
                                                             x, w.tmp.p);
   fold_sum(c, exact, w.tmp.p, n, dots + 6);
-  ++g_launches, recomb_finish_kernel<<<1, 1, 0, c.s>>>(dots, dots + 6, growth);
+  count_launch(), recomb_finish_kernel<<<1, 1, 0, c.s>>>(dots, dots + 6, growth);
   CK_LAUNCH();
   c.work += (double)cols * (double)n;
 }
@@ -244,6 +249,23 @@ struct Driver {
       relax_solve(c, L.op.view(), L.sched, L.color.get(), b, x, ws.lv[l].r, &sw, exact);
       relax_sweeps += sw;
     }
+  }
+
+  // the finest level's coarsened right-hand sides are cached for the whole
+  // solve (cycle.cpp:139-148); computing them before the first cycle keeps
+  // every cycle's kernel schedule identical
+  void prepare_top(const double* b) {
+    if (h.levels.size() < 2 || h.levels[1]->kind != KIND_ELIM || ws.top_rhs_valid) return;
+    const auto& st = h.levels[1]->stages;
+    const size_t S = st.size();
+    const double* in = b;
+    for (size_t s = 0; s < S; ++s) {
+      double* out = s + 1 < S ? ws.lv[0].stage_rhs[s + 1].p : ws.lv[1].b.p;
+      coarsen_rhs(c, st[s]->view(), in, out);
+      c.work += (double)st[s]->nnzf;
+      in = out;
+    }
+    ws.top_rhs_valid = true;
   }
 
   // cycle.cpp:131-164
@@ -368,7 +390,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   unsigned long long* bmax = (unsigned long long*)(c.dscal + 140);
   double* bsum = c.dscal + 141;
   CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), c.s));
-  ++g_launches, absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
+  count_launch(), absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
   CK_LAUNCH();
   // the compatibility test is a threshold decision: sequential in VALIDATE
   // mode (bit-exact with the reference), fixed-order tree otherwise
@@ -398,37 +420,80 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   const bool use_tail = !exact && cfg.correction == 0;
   if (use_tail && !ws.tail_built) {
     const char* env = getenv("LAMG_TAIL_ROWS");
-    ws.tail.build(c, h, ws, env ? atoi(env) : 20000);
+    ws.tail.build(c, h, ws, env ? atoi(env) : 40000);
     ws.tail_built = true;
   }
   if (!use_tail) ws.tail.first = 1 << 30;
   else ws.tail.reset(c);
   const double w0 = c.work = 0.0;
-  copy_d(c, x, x0, n);
+  // the solve runs on fixed-address copies of b and x (CUDA-graph replay)
+  double* xw = ws.lv[0].x.p;
+  const double* bw = ws.lv[0].b.p;
+  copy_d(c, ws.lv[0].b.p, b, n);
+  copy_d(c, xw, x0, n);
   double* rn_d = c.dscal + 150;
   double* growth = c.dscal + 151;
   CK(cudaMemsetAsync(growth, 0, sizeof(double), c.s));
   Driver d{c, h, cfg, ws, LevelCredits{}, exact, growth};
   d.credits.credit.assign(h.levels.size(), 0.0);
-  d.resid(0, b, x, ws.lv[0].r.p);
+  d.resid(0, bw, xw, ws.lv[0].r.p);
   fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
   const double r0 = read_scalar(c, rn_d);
   res.residuals.push_back(r0);
   if (r0 == 0.0) {
-    sub_mean(c, exact, x, n);
+    sub_mean(c, exact, xw, n);
+    copy_d(c, x, xw, n);
     c.sync();
     res.converged = true;
     res.acf = 0.0;
     res.solve_work = (c.work - w0) / (double)a.m;
     return LAMG_OK;
   }
+  // graphs need a host-sync-free cycle: flat correction, coarsest in the tail
+  const char* eg = getenv("LAMG_GRAPHS");
+  const bool use_graphs = use_tail && !c.prof.enabled && (int)h.levels.size() - 1 >= ws.tail.first &&
+                          !(eg && atoi(eg) == 0);
+  if (use_graphs) d.prepare_top(bw);
   const double target = r0 / cfg.target_reduction;
   int rc = LAMG_OK;
   for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
-    d.visit(0, b, x, 1);
-    sub_mean(c, exact, x, n);
-    d.resid(0, b, x, ws.lv[0].r.p);
-    fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
+    auto one_cycle = [&] {
+      d.visit(0, bw, xw, 1);
+      sub_mean(c, exact, xw, n);
+      d.resid(0, bw, xw, ws.lv[0].r.p);
+      fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
+    };
+    if (use_graphs) {
+      Workspace::CycleGraph* g = nullptr;
+      for (auto& e : ws.graphs)
+        if (e.key == d.credits.credit) g = &e;
+      if (!g) {
+        Workspace::CycleGraph e;
+        e.key = d.credits.credit;
+        const double wc = c.work;
+        const long long l0 = t_launches;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+        one_cycle();
+        CK(cudaStreamEndCapture(c.s, &graph));
+        CK(cudaGraphInstantiate(&e.exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        e.work = c.work - wc;
+        e.launches = t_launches - l0;
+        g_launches -= e.launches;  // counted when the graph runs
+        t_launches = l0;
+        e.credits_after = d.credits.credit;
+        c.work = wc;
+        ws.graphs.push_back(std::move(e));
+        g = &ws.graphs.back();
+      }
+      CK(cudaGraphLaunch(g->exec, c.s));
+      g_launches += g->launches;
+      c.work += g->work;
+      d.credits.credit = g->credits_after;
+    } else {
+      one_cycle();
+    }
     const double rn = read_scalar(c, rn_d);
     res.residuals.push_back(rn);
     res.cycles = cycle;
@@ -444,6 +509,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
       break;
     }
   }
+  copy_d(c, x, xw, n);
   if (rc == LAMG_OK) {
     const double rp = res.residuals.back();
     res.acf = std::pow(rp / r0, 1.0 / (double)res.cycles);

@@ -50,6 +50,17 @@ struct Workspace {
   bool top_rhs_valid = false;
   TailPlan tail;          // throughput mode: on-device coarse tail
   bool tail_built = false;
+  // throughput mode: one CUDA graph per host-level credit state; a cycle's
+  // kernel schedule depends only on the credits at its start
+  struct CycleGraph {
+    std::vector<double> key, credits_after;
+    cudaGraphExec_t exec = nullptr;
+    double work = 0.0;
+    long long launches = 0;  // kernels in the graph (counted on every replay)
+  };
+  std::vector<CycleGraph> graphs;
+  void clear_graphs();
+  ~Workspace() { clear_graphs(); }
   void ensure(Ctx& c, const DHier& h);
   void ensure_adaptive(Ctx& c, const DHier& h);
 };

@@ -30,10 +30,13 @@ struct BlockScope {
   __device__ static void sync() { __syncthreads(); }
   __device__ static bool leader() { return threadIdx.x == 0; }
 };
+// The tail grid is a single thread-block cluster: its barrier is the
+// hardware cluster barrier (barrier.cluster.arrive.release / wait.acquire),
+// an order of magnitude cheaper than a software grid barrier.
 struct GridScope {
   __device__ static int64_t tid() { return blockIdx.x * (int64_t)blockDim.x + threadIdx.x; }
   __device__ static int64_t stride() { return (int64_t)gridDim.x * blockDim.x; }
-  __device__ static void sync() { cg::this_grid().sync(); }
+  __device__ static void sync() { cg::this_cluster().sync(); }
   __device__ static bool leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
 };
 
@@ -127,7 +130,7 @@ constexpr int kMaxColors = 256;
 
 template <class S, int G>
 __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
-                                int32_t* s_cptr) {
+                                int32_t* s_cptr, TailCounters* ctr_dbg) {
   constexpr int U = G == 1 ? 8 : 4;
   const int nc = L.ncolors;
   const bool cached = nc < kMaxColors;
@@ -165,8 +168,11 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
     }
   };
   prefetch(0);
+  long long tA = clock64(), tB = 0, tC = 0, tD = 0;
+  long long acc_fold = 0, acc_extra = 0, acc_pre = 0, acc_bar = 0;
   for (int sw = 0; sw < sweeps; ++sw)
     for (int32_t cc = 0; cc < nc; ++cc) {
+      tA = clock64();
       const int32_t i0 = cached ? s_cptr[cc] : L.cptr[cc];
       const int32_t i1 = cached ? s_cptr[cc + 1] : L.cptr[cc + 1];
       {  // the prefetched row
@@ -191,6 +197,7 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
           if (p_ok && lane == 0) x[p_u] = (p_b - acc) / p_d;
         }
       }
+      tB = clock64();
       // rows beyond the first slot of this colour (large levels only)
       const int64_t span = ((int64_t)(i1 - i0) * G + 31) / 32 * 32;
       for (int64_t t = S::tid() + S::stride(); t < span; t += S::stride()) {
@@ -209,10 +216,24 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
           }
         }
       }
+      tC = clock64();
       const int next = cc + 1 < nc ? cc + 1 : (sw + 1 < sweeps ? 0 : -1);
       if (next >= 0) prefetch(next);
+      // force the prefetched loads to land before timing the barrier
+      if (p_ok && p_c[0] == -7) x[0] = p_v[0] + p_b;
+      tD = clock64();
       S::sync();
+      acc_fold += tB - tA;
+      acc_extra += tC - tB;
+      acc_pre += tD - tC;
+      acc_bar += clock64() - tD;
     }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && std::is_same<S, GridScope>::value) {
+    ctr_dbg->ph_fold += acc_fold;
+    ctr_dbg->ph_extra += acc_extra;
+    ctr_dbg->ph_prefetch += acc_pre;
+    ctr_dbg->ph_barrier += acc_bar;
+  }
 }
 
 template <class S>
@@ -225,9 +246,9 @@ __device__ inline void gs(const TLevel& L, const double* __restrict__ b, double*
     return;
   }
   const long long tg = clock64();
-  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps, s_cptr);
-  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps, s_cptr);
-  else gs_group<S, 1>(L, b, x, sweeps, s_cptr);
+  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps, s_cptr, ctr);
+  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps, s_cptr, ctr);
+  else gs_group<S, 1>(L, b, x, sweeps, s_cptr, ctr);
   if (S::leader()) {
     ctr->cyc_global_gs += clock64() - tg;
     ctr->global_phases += (long long)sweeps * L.ncolors;
@@ -501,7 +522,11 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
   }
 }
 
-__global__ void __launch_bounds__(kTailThreads) tail_kernel(const TLevel* __restrict__ levels, int nlevels, int l0,
+// MINB = 2 caps registers at 64 so two tail CTAs share an SM: best when
+// many right-hand sides run concurrently; MINB = 1 (126 registers, no
+// spills) gives the lowest single-solve latency. LAMG_TAIL_OCC selects.
+template <int MINB>
+__global__ void __launch_bounds__(kTailThreads, MINB) tail_kernel(const TLevel* __restrict__ levels, int nlevels, int l0,
                                                             int theta0, double* credits_g, double mu,
                                                             int32_t small_rows, double* part, TailCounters* ctr) {
   __shared__ double credits[kMaxLevels];
@@ -532,8 +557,10 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   }
   const char* e1 = getenv("LAMG_TAIL_SMALL");
   small_rows = e1 ? atoi(e1) : 4096;
+  const char* e3 = getenv("LAMG_TAIL_SMEM_KB");
+  smem = e3 ? std::min(kTailSmemMax, atoi(e3) * 1024) : 0;  // default: operators via L1/L2
   const char* e2 = getenv("LAMG_TAIL_CTAS");
-  ctas = std::max(1, std::min(e2 ? atoi(e2) : 64, c.sms));
+  ctas = std::max(1, std::min(e2 ? atoi(e2) : 8, 16));  // one cluster (<= 16 CTAs)
   std::vector<TLevel> tl(nl);
   for (int l = first; l < nl; ++l) {
     const DLevel& L = *h.levels[l];
@@ -563,7 +590,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
       t.pval = L.color->val.p;
       t.pdiag = L.color->diag.p;
       const int64_t bytes = (int64_t)a.n * (3 * 8 + 4 + 4) + 4 + 2 * a.m * 12 + 4 * (L.color->ncolors + 1);
-      t.smem_ok = bytes <= kTailSmem;
+      t.smem_ok = bytes <= smem;
     }
     if (L.direct) {
       const DDirect& d = *L.direct;
@@ -600,10 +627,29 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   CK(cudaMemcpyAsync(dlevels.p, tl.data(), sizeof(TLevel) * nl, cudaMemcpyHostToDevice, c.s));
   credits.alloc(nl, c.s);
   ctr.alloc(1, c.s);
-  CK(cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_kernel, kTailThreads, kTailSmem));
-  ctas = std::min(ctas, std::max(1, per_sm) * c.sms);
+  const char* e4 = getenv("LAMG_TAIL_OCC");
+  occ2 = !(e4 && atoi(e4) == 1);
+  kernel = occ2 ? (const void*)tail_kernel<2> : (const void*)tail_kernel<1>;
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax));
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // largest cluster the device can co-schedule with this footprint
+  while (ctas > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = ctas;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kernel, &cfg) == cudaSuccess && nclusters > 0) break;
+    cudaGetLastError();
+    ctas /= 2;
+  }
   part.alloc(std::max(ctas, 1), c.s);
   c.sync();
 }
@@ -620,8 +666,21 @@ void TailPlan::run(Ctx& c, int l, int theta, double mu, int nlevels) {
   double* pt = part.p;
   TailCounters* ct = ctr.p;
   int32_t sr = small_rows;
-  void* args[] = {(void*)&lv, &nlevels, &l, &theta, &cr, &mu, &sr, &pt, &ct};
-  coop_launch(c, (const void*)tail_kernel, ctas, kTailThreads, args, kTailSmem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = ctas;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  if (occ2) CK(cudaLaunchKernelEx(&cfg, tail_kernel<2>, lv, nlevels, l, theta, cr, mu, sr, pt, ct));
+  else CK(cudaLaunchKernelEx(&cfg, tail_kernel<1>, lv, nlevels, l, theta, cr, mu, sr, pt, ct));
 }
 
 void TailPlan::collect(Ctx& c, double* work, int* relax_sweeps) {
@@ -639,6 +698,10 @@ void TailPlan::collect(Ctx& c, double* work, int* relax_sweeps) {
             h.smem_calls ? (double)h.cyc_stage / h.smem_calls : 0.0,
             h.smem_phases ? (double)h.cyc_phases / h.smem_phases : 0.0, h.global_phases,
             h.global_phases ? (double)h.cyc_global_gs / h.global_phases : 0.0);
+  if (getenv("LAMG_TAIL_DEBUG") && h.global_phases)
+    fprintf(stderr, "[tail] grid phase breakdown (CTA0 thread0, cycles/phase): fold %.0f extra %.0f prefetch %.0f barrier %.0f\n",
+            (double)h.ph_fold / h.global_phases, (double)h.ph_extra / h.global_phases,
+            (double)h.ph_prefetch / h.global_phases, (double)h.ph_barrier / h.global_phases);
 }
 
 }  // namespace lamgb

@@ -9,7 +9,7 @@ namespace lamgb {
 
 constexpr int kMaxLevels = 64;
 constexpr int kMaxStages = 8;
-constexpr int kTailSmem = 200 * 1024;  // dynamic shared memory of the tail CTA
+constexpr int kTailSmemMax = 200 * 1024;  // dynamic shared memory of the tail CTA (upper bound)
 
 struct TailCounters {
   double work;          // edge units (exact integers: order-free)
@@ -17,6 +17,7 @@ struct TailCounters {
   long long phases;     // diagnostics: colour phases, total cycles, GS cycles
   long long cyc_total, cyc_gs;
   long long smem_calls, smem_phases, cyc_stage, cyc_phases, cyc_global_gs, global_phases;
+  long long ph_fold, ph_extra, ph_prefetch, ph_barrier;
 };
 
 // one level as the tail kernel sees it: operator (natural + colour-permuted),
@@ -71,6 +72,9 @@ struct TailPlan {
   int first = 1 << 30;  // first level handled on-device (>= nlevels: none)
   int32_t small_rows = 4096;  // levels this small run in CTA 0 alone
   int ctas = 64;
+  int smem = kTailSmemMax;  // bytes of dynamic shared memory per tail CTA
+  bool occ2 = true;         // two tail CTAs per SM (64-register variant)
+  const void* kernel = nullptr;
   DVec<TLevel> dlevels;
   DVec<double> credits;
   DVec<double> part;

@@ -87,20 +87,20 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   const int32_t ncol = reduce_max_i32(c, color.p, n) + 1;
   DVec<int32_t> ids(n, c.s);
   DVec<uint32_t> ks(n, c.s);
-  ++g_launches, iota32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
+  count_launch(), iota32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(ids.p, n);
   CK_LAUNCH();
   out.row_ids.alloc(n, c.s);
   int bits = 1;
   while ((1 << bits) <= ncol && bits < 31) ++bits;
   sort_pairs_u32_i32(c, (const uint32_t*)color.p, ks.p, ids.p, out.row_ids.p, n, bits);
   DVec<int32_t> cptr(ncol + 1, c.s);
-  ++g_launches, color_bounds_kernel<<<blocks_for(n + 1), kThreads, 0, c.s>>>(ks.p, n, ncol, cptr.p);
+  count_launch(), color_bounds_kernel<<<blocks_for(n + 1), kThreads, 0, c.s>>>(ks.p, n, ncol, cptr.p);
   CK_LAUNCH();
   out.ncolors = ncol;
   out.group = row_group_for(a.n, a.m);
   out.cptr_h = cptr.to_host();
   DVec<int64_t> deg(n + 1, c.s);
-  ++g_launches, perm_deg_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, deg.p);
+  count_launch(), perm_deg_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, deg.p);
   CK_LAUNCH();
   CK(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), c.s));
   out.rp.alloc(n + 1, c.s);
@@ -108,7 +108,7 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   out.col.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
   out.val.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
   out.diag.alloc(n, c.s);
-  ++g_launches, perm_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
+  count_launch(), perm_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
                                                                      out.val.p, out.diag.p);
   CK_LAUNCH();
 }
@@ -158,8 +158,8 @@ void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double
     return;
   }
   const int64_t threads = (int64_t)a.n * group;
-  if (group == 4) ++g_launches, residual_group_kernel<4><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
-  else ++g_launches, residual_group_kernel<8><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
+  if (group == 4) count_launch(), residual_group_kernel<4><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
+  else count_launch(), residual_group_kernel<8><<<blocks_for(threads), kThreads, 0, c.s>>>(a, b, x, r);
   CK_LAUNCH();
 }
 
@@ -184,7 +184,7 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
   if (n <= 16384) {
     // device copy of the colour pointers lives right after the permuted rp
     static_assert(sizeof(int64_t) >= sizeof(int32_t), "");
-    ++g_launches, gs_color_cta_kernel<<<1, 1024, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
+    count_launch(), gs_color_cta_kernel<<<1, 1024, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
                                                            (const int32_t*)(cl.rp.p + n + 1), cl.ncolors, b, x,
                                                            sweeps);
     CK_LAUNCH();
@@ -196,13 +196,13 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
       if (i1 <= i0) continue;
       const int64_t rows = i1 - i0;
       if (cl.group == 1)
-        ++g_launches, gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
+        count_launch(), gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
                                                                              cl.row_ids.p, b, x, i0, i1);
       else if (cl.group == 4)
-        ++g_launches, gs_color_group_kernel<4><<<blocks_for(rows * 4), kThreads, 0, c.s>>>(
+        count_launch(), gs_color_group_kernel<4><<<blocks_for(rows * 4), kThreads, 0, c.s>>>(
             cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
       else
-        ++g_launches, gs_color_group_kernel<8><<<blocks_for(rows * 8), kThreads, 0, c.s>>>(
+        count_launch(), gs_color_group_kernel<8><<<blocks_for(rows * 8), kThreads, 0, c.s>>>(
             cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
     }
   CK_LAUNCH();
@@ -242,7 +242,7 @@ void build_direct_inverse(Ctx& c, DDirect& d) {
   DVec<double> work((int64_t)d.maxN * d.maxN + 1, c.s);
   for (int32_t ci = 0; ci < d.ncomp; ++ci) {
     const int32_t N = d.comp_size[ci] + 1;
-    ++g_launches, lu_inverse_kernel<<<blocks_for(N), 128, 0, c.s>>>(d.lu.p + off[ci], d.perm.p + start[ci] + ci, N,
+    count_launch(), lu_inverse_kernel<<<blocks_for(N), 128, 0, c.s>>>(d.lu.p + off[ci], d.perm.p + start[ci] + ci, N,
                                                                    d.inv.p + ioff[ci], work.p);
     CK_LAUNCH();
     c.sync();
