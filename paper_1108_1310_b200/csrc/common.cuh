@@ -305,6 +305,59 @@ __device__ __forceinline__ double group_dot(const int32_t* __restrict__ col, con
   return p;
 }
 
+// Heavy-row dot product by a whole CTA (hub rows of power-law graphs):
+// strided partials, fixed-order block tree. Every thread gets the sum.
+__device__ __forceinline__ double block_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
+                                            const double* x, int64_t b, int64_t e) {
+  __shared__ double sh_bd[33];
+  double p = 0.0;
+  for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) p += __ldcs(val + k) * x[__ldcs(col + k)];
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_down_sync(0xffffffffu, p, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh_bd[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh_bd[w];
+    sh_bd[32] = t;
+  }
+  __syncthreads();
+  return sh_bd[32];
+}
+
+// VALIDATE-mode heavy row: s (-|+)= val[k]*x[col[k]] for k in [b,e) in k
+// order, bit-identical to the sequential loop. The CTA computes the products
+// (each rounded exactly as in the loop) in parallel chunks through shared
+// memory; thread 0 runs the dependent add chain. Every thread gets s.
+// x == nullptr folds val[k] itself.
+// `xs`/`xk` select column k of a node-major block (x[col*xs + xk]).
+template <bool SUB>
+__device__ __forceinline__ double block_seq_fold(double s, const int32_t* __restrict__ col,
+                                                 const double* __restrict__ val, const double* x, int64_t b,
+                                                 int64_t e, int xs = 1, int xk = 0) {
+  __shared__ double sh_prod[256];
+  __shared__ double sh_s;
+  if (threadIdx.x == 0) sh_s = s;
+  for (int64_t c0 = b; c0 < e; c0 += 256) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) {
+      const int64_t k = c0 + j;
+      sh_prod[j] = k < e ? (x ? val[k] * x[(int64_t)col[k] * xs + xk] : val[k]) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int cnt = e - c0 < 256 ? (int)(e - c0) : 256;
+      double t = sh_s;
+      for (int j = 0; j < cnt; ++j) t = SUB ? t - sh_prod[j] : t + sh_prod[j];
+      sh_s = t;
+    }
+  }
+  __syncthreads();
+  const double r = sh_s;
+  __syncthreads();
+  return r;
+}
+
 // launches a kernel cooperatively (all blocks co-resident)
 void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** args, size_t smem = 0);
 

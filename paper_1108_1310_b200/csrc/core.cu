@@ -12,17 +12,41 @@ namespace lamgb {
 // ------------------------------------------------------------- residual
 // thread per row; the row fold runs in column order (sparse_laplacian.cpp:156-160)
 __global__ void residual_exact_kernel(CSRv a, const double* __restrict__ b,
-                                      const double* __restrict__ x, double* __restrict__ r) {
+                                      const double* __restrict__ x, double* __restrict__ r, bool skip_heavy) {
   int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= a.n) return;
+  if (skip_heavy && a.rp[u + 1] - a.rp[u] > kHeavyRowExact) return;
   double s = a.diag[u] * x[u];
   s = row_fold<8, false, true>(s, a.col, a.val, x, a.rp[u], a.rp[u + 1]);
   r[u] = b ? b[u] - s : s;
 }
 
-void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r) {
+__global__ void residual_heavy_exact_kernel(CSRv a, const int32_t* heavy, const double* __restrict__ b,
+                                            const double* __restrict__ x, double* __restrict__ r) {
+  const int32_t u = heavy[blockIdx.x];
+  const double s = block_seq_fold<false>(a.diag[u] * x[u], a.col, a.val, x, a.rp[u], a.rp[u + 1]);
+  if (threadIdx.x == 0) r[u] = b ? b[u] - s : s;
+}
+
+__global__ void heavy_flag_rows_kernel(CSRv a, uint8_t* f) {
+  int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < a.n) f[u] = a.rp[u + 1] - a.rp[u] > kHeavyRowExact;
+}
+
+int32_t heavy_rows(Ctx& c, const CSRv& a, DVec<int32_t>& out) {
+  out.alloc(std::max(a.n, 1), c.s);
+  if (a.n == 0) return 0;
+  DVec<uint8_t> f(a.n, c.s);
+  count_launch(), heavy_flag_rows_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, f.p);
+  CK_LAUNCH();
+  return (int32_t)select_flagged_index(c, f.p, out.p, a.n);
+}
+
+void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, const int32_t* heavy,
+                    int32_t nheavy) {
   if (a.n == 0) return;
-  count_launch(), residual_exact_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, b, x, r);
+  count_launch(), residual_exact_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, b, x, r, nheavy > 0);
+  if (nheavy) count_launch(), residual_heavy_exact_kernel<<<nheavy, 256, 0, c.s>>>(a, heavy, b, x, r);
   CK_LAUNCH();
 }
 
@@ -30,12 +54,15 @@ void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, dou
 __global__ void deps_kernel(CSRv a, bool backward, int32_t* cnt) {
   int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= a.n) return;
-  int32_t c = 0;
-  for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
-    int32_t v = a.col[k];
-    c += backward ? (v > u) : (v < u);
+  // rows are sorted: the lower neighbours are the prefix below u
+  int64_t lo = a.rp[u], hi = a.rp[u + 1];
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (a.col[mid] < u) lo = mid + 1;
+    else hi = mid;
   }
-  cnt[u] = c;
+  const int64_t lower = lo - a.rp[u];
+  cnt[u] = (int32_t)(backward ? (a.rp[u + 1] - a.rp[u]) - lower : lower);
 }
 
 __global__ void zero_dep_flags_kernel(const int32_t* cnt, int32_t n, uint8_t* flag) {
@@ -50,12 +77,16 @@ __global__ void kahn_kernel(CSRv a, bool backward, int32_t* cnt, int32_t* level,
                             int32_t* ctl /* [0]=tail, [1]=nfronts */, int32_t first_count) {
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  // one warp per finished row: hubs release their many later neighbours
+  // with 32 lanes instead of one thread
+  const int64_t gwarp = gtid >> 5, nwarps = gstride >> 5;
+  const int lane = threadIdx.x & 31;
   int32_t fs = 0, fe = first_count, r = 0;
   while (fs < fe) {
-    for (int64_t i = fs + gtid; i < fe; i += gstride) {
+    for (int64_t i = fs + gwarp; i < fe; i += nwarps) {
       int32_t u = queue[i];
-      level[u] = r;
-      for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
+      if (lane == 0) level[u] = r;
+      for (int64_t k = a.rp[u] + lane; k < a.rp[u + 1]; k += 32) {
         int32_t v = a.col[k];
         bool later = backward ? (v < u) : (v > u);
         if (later && atomicSub(&cnt[v], 1) == 1) queue[atomicAdd(&ctl[0], 1)] = v;
@@ -76,6 +107,11 @@ __global__ void front_bounds_kernel(const uint32_t* lvl_sorted, int32_t n, int32
   if (i >= n) return;
   if (i == 0 || lvl_sorted[i] != lvl_sorted[i - 1]) front_ptr[lvl_sorted[i]] = i;
   if (i == 0) front_ptr[nfronts] = n;
+}
+
+__global__ void heavy_pos_kernel(CSRv a, const int32_t* rows, int32_t n, uint8_t* f) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = a.rp[rows[i] + 1] - a.rp[rows[i]] > kHeavyRowExact;
 }
 
 __global__ void iota_kernel(int32_t* x, int64_t n) {
@@ -122,6 +158,23 @@ void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
   int32_t w = 0;
   for (int32_t f = 0; f < nf; ++f) w = std::max(w, fp[f + 1] - fp[f]);
   out.max_width = w;
+  // heavy rows in sweep order, grouped by front
+  DVec<uint8_t> hf(n, c.s);
+  count_launch(), heavy_pos_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.rows.p, n, hf.p);
+  CK_LAUNCH();
+  out.heavy.alloc(n, c.s);
+  out.nheavy = (int32_t)select_flagged_index(c, hf.p, out.heavy.p, n);
+  std::vector<int32_t> hp(nf + 1, 0);
+  if (out.nheavy) {
+    std::vector<int32_t> hv(out.nheavy);
+    out.heavy.download(hv.data(), out.nheavy);
+    c.sync();
+    for (int32_t f = 0; f <= nf; ++f) hp[f] = (int32_t)(std::lower_bound(hv.begin(), hv.end(), fp[f]) - hv.begin());
+  }
+  out.heavy_ptr.alloc(nf + 1, c.s);
+  out.heavy_ptr.upload(hp.data(), nf + 1);
+  out.nheavy_nat = heavy_rows(c, a, out.heavy_nat);
+  c.sync();
 }
 
 // One persistent launch per sweep set: rows of a front update in parallel,
@@ -129,15 +182,32 @@ void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
 // value loads for all K vectors.
 __global__ void gs_fronts_kernel(CSRv a, const double* __restrict__ b, double* x, int K,
                                  const int32_t* __restrict__ front_ptr, const int32_t* __restrict__ rows,
-                                 int32_t nfronts, int sweeps, int backward, DevErr* err) {
+                                 int32_t nfronts, int sweeps, int backward, DevErr* err,
+                                 const int32_t* __restrict__ heavy, const int32_t* __restrict__ heavy_ptr) {
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int32_t f = 0; f < nfronts; ++f) {
       const int32_t fs = front_ptr[f], fe = front_ptr[f + 1];
+      // heavy rows of this front: one CTA each, bit-exact sequential fold
+      for (int32_t h = heavy_ptr[f] + blockIdx.x; h < heavy_ptr[f + 1]; h += gridDim.x) {
+        const int32_t u = rows[heavy[h]];
+        const double d = a.diag[u];
+        for (int kk = 0; kk < K; ++kk) {
+          const double s = block_seq_fold<true>(b ? b[(int64_t)u * K + kk] : 0.0, a.col, a.val, x, a.rp[u],
+                                                a.rp[u + 1], K, kk);
+          if (threadIdx.x == 0) {
+            if (d != 0.0) x[(int64_t)u * K + kk] = s / d;
+            else
+              dev_report(err, backward ? (unsigned long long)(a.n - 1 - u) : (unsigned long long)u,
+                         DE_GS_SINGULAR, u, 0);
+          }
+        }
+      }
       for (int64_t i = fs + gtid / K; i < fe; i += gstride / K) {
         const int kk = (int)(gtid % K);
         const int32_t u = rows[i];
+        if (a.rp[u + 1] - a.rp[u] > kHeavyRowExact) continue;
         double s = b ? b[(int64_t)u * K + kk] : 0.0;
         const int64_t e = a.rp[u + 1];
         if (K == 1) s = row_fold<8, true>(s, a.col, a.val, x, a.rp[u], e);
@@ -172,7 +242,9 @@ void gs_exact(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, doubl
   int32_t nf = sch.nfronts;
   int bw = backward ? 1 : 0;
   int t = (threads / K) * K;  // (row, k) pairs tile the grid exactly
-  void* args[] = {&av, (void*)&b, &x, &K, (void*)&fp, (void*)&rw, &nf, &sweeps, &bw, &c.derr};
+  const int32_t* hv = sch.heavy.p;
+  const int32_t* hp = sch.heavy_ptr.p;
+  void* args[] = {&av, (void*)&b, &x, &K, (void*)&fp, (void*)&rw, &nf, &sweeps, &bw, &c.derr, (void*)&hv, (void*)&hp};
   if (check) c.checked([&] { coop_launch(c, (const void*)gs_fronts_kernel, blocks, t, args); });
   else coop_launch(c, (const void*)gs_fronts_kernel, blocks, t, args);
 }
@@ -307,6 +379,7 @@ __device__ inline unsigned long long vkey(int32_t u, int64_t pos, int sub) {
 __global__ void validate_kernel(CSRv a, const unsigned long long* maxdiag_bits, DevErr* err) {
   int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= a.n) return;
+  if (a.rp[u + 1] - a.rp[u] > kHeavyRowExact) return;  // validate_heavy_kernel
   const double md = __longlong_as_double((long long)*maxdiag_bits);
   const double tol = 1e-10 * (md < 1e-300 ? 1e-300 : md);
   double row_sum = a.diag[u];
@@ -331,14 +404,58 @@ __global__ void validate_kernel(CSRv a, const unsigned long long* maxdiag_bits, 
   if (e > b && a.diag[u] <= 0.0) dev_report(err, vkey(u, e - b, 6), DE_VAL_DIAG, u, 0);
 }
 
+// hub rows: one CTA per row; entry checks in parallel (the minimum key is
+// the first failure, as in the sequential scan), row sum folded in order
+__global__ void validate_heavy_kernel(CSRv a, const int32_t* heavy, const unsigned long long* maxdiag_bits,
+                                      DevErr* err) {
+  const int32_t u = heavy[blockIdx.x];
+  const double md = __longlong_as_double((long long)*maxdiag_bits);
+  const double tol = 1e-10 * (md < 1e-300 ? 1e-300 : md);
+  const int64_t b = a.rp[u], e = a.rp[u + 1];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) {
+    const int32_t v = a.col[k];
+    const int64_t pos = k - b;
+    int kind = -1;
+    if (v == u) kind = DE_VAL_SELF;
+    else if (v < 0 || v >= a.n) kind = DE_VAL_RANGE;
+    else if (k > b && a.col[k - 1] >= v) kind = DE_VAL_SORT;
+    else {
+      int64_t lo = a.rp[v], hi = a.rp[v + 1];
+      while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (a.col[mid] < u) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo == a.rp[v + 1] || a.col[lo] != u) kind = DE_VAL_STRUCT;
+      else if (a.val[lo] != a.val[k]) kind = DE_VAL_VALUE;
+    }
+    if (kind >= 0) {
+      dev_report(err, vkey(u, pos, kind - DE_VAL_SELF), kind, u, v);
+      bad = 1;
+    }
+  }
+  __syncthreads();
+  if (bad) return;
+  const double row_sum = block_seq_fold<false>(a.diag[u], a.col, a.val, nullptr, b, e);
+  if (threadIdx.x != 0) return;
+  if (fabs(row_sum) > tol) { dev_report(err, vkey(u, e - b, 5), DE_VAL_ROWSUM, u, 0, row_sum); return; }
+  if (e > b && a.diag[u] <= 0.0) dev_report(err, vkey(u, e - b, 6), DE_VAL_DIAG, u, 0);
+}
+
 void validate_exact(Ctx& c, const CSRv& a) {
   if (a.n <= 0) throw LamgError(LAMG_E_INVALID_LAPLACIAN, "empty matrix");
   unsigned long long* md = (unsigned long long*)(c.dscal + 90);
   CK(cudaMemsetAsync(md, 0, sizeof(unsigned long long), c.s));
   count_launch(), abs_max_kernel<<<std::min(blocks_for(a.n), 1024), kThreads, 0, c.s>>>(a.diag, a.n, md);
   CK_LAUNCH();
+  DVec<int32_t> heavy;
+  const int32_t nh = heavy_rows(c, a, heavy);
   c.checked([&] {
     count_launch(), validate_kernel<<<blocks_for(a.n), kThreads, 0, c.s>>>(a, md, c.derr);
+    if (nh) count_launch(), validate_heavy_kernel<<<nh, 256, 0, c.s>>>(a, heavy.p, md, c.derr);
     CK_LAUNCH();
   });
 }

@@ -16,13 +16,23 @@ struct Schedule {
   int32_t max_width = 0;
   DVec<int32_t> front_ptr;  // [nfronts+1]
   DVec<int32_t> rows;       // [n] rows, ascending within a front
+  // heavy rows (hubs) are swept by a whole CTA: positions into `rows`,
+  // grouped by front, with per-front ranges
+  DVec<int32_t> heavy;
+  DVec<int32_t> heavy_ptr;  // [nfronts+1]
+  int32_t nheavy = 0;
+  DVec<int32_t> heavy_nat;  // the same rows in natural order (residuals)
+  int32_t nheavy_nat = 0;
 };
 
 void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out);
 
 // r = b - A x (residual, sparse_laplacian.cpp:170-175); b == nullptr gives y = A x
 // (mvm, :151-162). Per-row fold in column order: bit-exact.
-void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r);
+void residual_exact(Ctx& c, const CSRv& a, const double* b, const double* x, double* r,
+                    const int32_t* heavy = nullptr, int32_t nheavy = 0);
+// natural rows with more than kHeavyRow entries (ascending)
+int32_t heavy_rows(Ctx& c, const CSRv& a, DVec<int32_t>& out);
 
 // Gauss-Seidel sweep(s) over the schedule (smoothing.cpp:13-40). x is n*K
 // node-major (K independent right-hand sides / test vectors); b may be null
@@ -40,6 +50,7 @@ struct UpperIndex {  // entries with col > row, in CSR order
   DVec<int32_t> row;
 };
 void build_upper_index(Ctx& c, const CSRv& a, UpperIndex& out);
+constexpr int64_t kHeavyRowExact = 2048;
 void energy_seq(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, double* d_out,
                 DVec<double>& scratch);
 

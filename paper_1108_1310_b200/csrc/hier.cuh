@@ -70,7 +70,15 @@ struct DColor {
   DVec<int32_t> col;            // natural column indices
   DVec<double> val;
   DVec<double> diag;            // diag of each stored row
+  // heavy rows (hubs: more than kHeavyRow entries) are reduced by a whole CTA
+  DVec<int32_t> heavy;          // stored positions of heavy rows, ascending
+  std::vector<int32_t> hptr_h;  // [ncolors+1] ranges of `heavy` per colour
+  DVec<int32_t> hptr;
+  DVec<int32_t> heavy_nat;      // natural rows with more than kHeavyRow entries
+  int32_t nheavy_nat = 0;
 };
+
+constexpr int64_t kHeavyRow = 2048;
 
 struct DLevel {
   int kind = KIND_FINEST;
@@ -146,12 +154,14 @@ void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, 
 void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out);
 void gs_colored(Ctx& c, const DColor& col, int32_t n, const double* b, double* x, int sweeps);
 // throughput residual r = b - A x with `group` lanes per row (tree-folded rows)
-void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, int group);
+void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, const DColor& cl);
 inline int row_group_for(int64_t n, int64_t m) {
   const double deg = n ? 2.0 * (double)m / (double)n : 0.0;
   return deg < 8.0 ? 1 : 8;
 }
 void build_direct_inverse(Ctx& c, DDirect& d);
+// whole relaxation-coarsest solve in one cooperative launch; returns sweeps
+int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const double* b, double* x, double* r);
 void prepare_throughput(Ctx& c, DHier& h);
 
 }  // namespace lamgb

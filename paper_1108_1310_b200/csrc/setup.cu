@@ -1134,8 +1134,14 @@ void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exa
 void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const double* b,
                  double* x, DVec<double>& r, int* sweeps_out, bool exact) {
   if (r.n < a.n) r.alloc(a.n, c.s);
+  if (!exact && col) {
+    const int sw = relax_colored_coop(c, a, *col, b, x, r.p);
+    c.work += (double)a.m * (1.0 + 2.0 * sw);
+    *sweeps_out = sw;
+    return;
+  }
   double* nrm = c.dscal + 110;
-  residual_exact(c, a, b, x, r.p);
+  residual_exact(c, a, b, x, r.p, sch.heavy_nat.p, sch.nheavy_nat);
   c.work += (double)a.m;
   seq_norm2(c, r.p, a.n, nrm);
   const double r0 = read_scalar(c, nrm);
@@ -1148,7 +1154,7 @@ void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, 
     c.work += (double)a.m;
     if (exact) subtract_mean_seq(c, x, a.n);
     else subtract_mean_tree(c, x, a.n);
-    residual_exact(c, a, b, x, r.p);
+    residual_exact(c, a, b, x, r.p, sch.heavy_nat.p, sch.nheavy_nat);
     c.work += (double)a.m;
     if (exact) seq_norm2(c, r.p, a.n, nrm);
     else tree_norm2(c, r.p, a.n, nrm);

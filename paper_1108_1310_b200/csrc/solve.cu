@@ -175,9 +175,10 @@ __global__ void recomb_finish_kernel(const double* dots, const double* new2, dou
 
 // recombine (cycle.cpp:23-103) with the reference's fold order in every dot
 static void recombine(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS& w, double* x,
-                      bool exact, double* growth) {
+                      bool exact, double* growth, const Schedule* sch = nullptr) {
   const int64_t n = a.n;
-  residual_exact(c, a, b, x, w.r.p);
+  if (sch) residual_exact(c, a, b, x, w.r.p, sch->heavy_nat.p, sch->nheavy_nat);
+  else residual_exact(c, a, b, x, w.r.p);
   c.work += (double)a.m;
   double* dots = c.dscal + 120;  // [120..126]
   CK(cudaMemsetAsync(dots, 0, 7 * sizeof(double), c.s));
@@ -319,8 +320,8 @@ struct Driver {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
-    if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, L.color->group);
-    else residual_exact(c, L.op.view(), b, x, r);
+    if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
+    else residual_exact(c, L.op.view(), b, x, r, L.sched.heavy_nat.p, L.sched.nheavy_nat);
     if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 40.0 * L.op.n + 8.0);
     c.work += (double)L.op.m;
   }
@@ -351,7 +352,7 @@ struct Driver {
       if (child.nu_post) gs(l, b, x, child.nu_post);
     }
     if (adaptive && nsaved > 0) {
-      recombine(c, L.op.view(), b, nsaved, w, x, exact, growth);
+      recombine(c, L.op.view(), b, nsaved, w, x, exact, growth, &L.sched);
       ++recombinations;
     }
   }

@@ -70,6 +70,11 @@ __global__ void perm_fill_kernel(CSRv a, const int32_t* row_ids, const int64_t* 
   pdiag[i] = a.diag[u];
 }
 
+__global__ void heavy_flags_kernel(const int64_t* rp, int32_t n, uint8_t* f) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = rp[i + 1] - rp[i] > kHeavyRow;
+}
+
 void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   const int32_t n = a.n;
   DVec<int32_t> color(n, c.s);
@@ -111,6 +116,28 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   count_launch(), perm_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
                                                                      out.val.p, out.diag.p);
   CK_LAUNCH();
+  // heavy rows: per colour (stored positions) and in natural order
+  DVec<uint8_t> hf(n, c.s);
+  count_launch(), heavy_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(out.rp.p, n, hf.p);
+  CK_LAUNCH();
+  out.heavy.alloc(n, c.s);
+  const int64_t nh = select_flagged_index(c, hf.p, out.heavy.p, n);
+  out.hptr_h.assign(ncol + 1, 0);
+  if (nh) {
+    std::vector<int32_t> hv((size_t)nh);
+    out.heavy.download(hv.data(), nh);
+    c.sync();
+    for (int32_t cc = 0; cc <= ncol; ++cc)
+      out.hptr_h[cc] = (int32_t)(std::lower_bound(hv.begin(), hv.end(), out.cptr_h[cc]) - hv.begin());
+    out.group = 8;
+  }
+  out.hptr.alloc(ncol + 1, c.s);
+  out.hptr.upload(out.hptr_h.data(), ncol + 1);
+  count_launch(), heavy_flags_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a.rp, n, hf.p);
+  CK_LAUNCH();
+  out.heavy_nat.alloc(n, c.s);
+  out.nheavy_nat = (int32_t)select_flagged_index(c, hf.p, out.heavy_nat.p, n);
+  c.sync();
 }
 
 // One colour: rows [i0, i1) of the permuted operator update in parallel.
@@ -134,7 +161,7 @@ __global__ void gs_color_group_kernel(const int64_t* __restrict__ rp, const int3
                                       double* x, int32_t i0, int32_t i1) {
   const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int64_t i = i0 + gid;
-  const bool ok = i < i1;
+  const bool ok = i < i1 && rp[i + 1] - rp[i] <= kHeavyRow;
   const double dot = group_dot<G>(col, val, x, ok ? rp[i] : 0, ok ? rp[i + 1] : 0);
   if (ok && (threadIdx.x & (G - 1)) == 0) {
     const int32_t u = row_ids[i];
@@ -146,13 +173,35 @@ template <int G>
 __global__ void residual_group_kernel(CSRv a, const double* __restrict__ b, const double* __restrict__ x,
                                       double* __restrict__ r) {
   const int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  const bool ok = u < a.n;
+  const bool ok = u < a.n && a.rp[u + 1] - a.rp[u] <= kHeavyRow;
   const double dot = group_dot<G>(a.col, a.val, x, ok ? a.rp[u] : 0, ok ? a.rp[u + 1] : 0);
   if (ok && (threadIdx.x & (G - 1)) == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
 }
 
-void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, int group) {
+// one CTA per heavy row (stored position list) of one colour
+__global__ void gs_heavy_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const double* __restrict__ val, const double* __restrict__ diag,
+                                const int32_t* __restrict__ row_ids, const int32_t* __restrict__ heavy,
+                                const double* __restrict__ b, double* x) {
+  const int32_t i = heavy[blockIdx.x];
+  const double dot = block_dot(col, val, x, rp[i], rp[i + 1]);
+  if (threadIdx.x == 0) {
+    const int32_t u = row_ids[i];
+    x[u] = (b[u] - dot) / diag[i];
+  }
+}
+__global__ void residual_heavy_kernel(CSRv a, const int32_t* __restrict__ heavy, const double* __restrict__ b,
+                                      const double* x, double* r) {
+  const int32_t u = heavy[blockIdx.x];
+  const double dot = block_dot(a.col, a.val, x, a.rp[u], a.rp[u + 1]);
+  if (threadIdx.x == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
+}
+
+void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, const DColor& cl) {
+  const int group = cl.group;
   if (a.n == 0) return;
+  if (cl.nheavy_nat)
+    count_launch(), residual_heavy_kernel<<<cl.nheavy_nat, 256, 0, c.s>>>(a, cl.heavy_nat.p, b, x, r);
   if (group == 1) {
     residual_exact(c, a, b, x, r);
     return;
@@ -195,6 +244,10 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
       int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
       if (i1 <= i0) continue;
       const int64_t rows = i1 - i0;
+      const int32_t nh = cl.hptr_h.empty() ? 0 : cl.hptr_h[cc + 1] - cl.hptr_h[cc];
+      if (nh)
+        count_launch(), gs_heavy_kernel<<<nh, 256, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
+                                                             cl.heavy.p + cl.hptr_h[cc], b, x);
       if (cl.group == 1)
         count_launch(), gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
                                                                              cl.row_ids.p, b, x, i0, i1);
@@ -206,6 +259,131 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
             cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
     }
   CK_LAUNCH();
+}
+
+// RelaxationSolver::solve (coarse_solver.cpp:82-93) for THROUGHPUT mode in
+// ONE cooperative launch: coloured sweeps separated by grid barriers, fixed-
+// order tree reductions (block partials summed in block order by every
+// thread), the convergence test on the device. Power-law hierarchies end in a
+// multi-million-row relaxation coarsest with hundreds of colours; host-driven
+// that is a launch per colour plus a host round trip per sweep.
+template <int G>
+__device__ inline void coop_residual(const CSRv& a, const double* __restrict__ b, const double* x, double* r,
+                                     const int32_t* heavy_nat, int32_t nheavy) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t h = blockIdx.x; h < nheavy; h += gridDim.x) {
+    const int32_t u = heavy_nat[h];
+    const double dot = block_dot(a.col, a.val, x, a.rp[u], a.rp[u + 1]);
+    if (threadIdx.x == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
+  }
+  const int64_t span = ((int64_t)a.n * G + 31) / 32 * 32;
+  for (int64_t t = gtid; t < span; t += gstride) {
+    const int64_t u = t / G;
+    const bool ok = u < a.n && a.rp[u + 1] - a.rp[u] <= kHeavyRow;
+    const double dot = group_dot<G, true>(a.col, a.val, x, ok ? a.rp[u] : 0, ok ? a.rp[u + 1] : 0);
+    if (ok && (threadIdx.x & (G - 1)) == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
+  }
+}
+
+__device__ inline double coop_sum(double v, double* part) {
+  __shared__ double sh[33];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    part[blockIdx.x] = t;
+  }
+  cg::this_grid().sync();
+  double t = 0.0;
+  for (unsigned g = 0; g < gridDim.x; ++g) t += ((volatile double*)part)[g];
+  cg::this_grid().sync();
+  return t;
+}
+
+template <int G>
+__global__ void relax_coop_kernel(CSRv a, const int64_t* __restrict__ prp, const int32_t* __restrict__ pcol,
+                                  const double* __restrict__ pval, const double* __restrict__ pdiag,
+                                  const int32_t* __restrict__ row_ids, const int32_t* __restrict__ cptr,
+                                  int32_t ncolors, const int32_t* __restrict__ heavy,
+                                  const int32_t* __restrict__ hptr, const int32_t* __restrict__ heavy_nat,
+                                  int32_t nheavy_nat, const double* __restrict__ b, double* x, double* r,
+                                  double* part, int* sweeps_out) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  coop_residual<G>(a, b, x, r, heavy_nat, nheavy_nat);
+  cg::this_grid().sync();
+  double loc = 0.0;
+  for (int64_t u = gtid; u < a.n; u += gstride) loc += r[u] * r[u];
+  const double r0 = sqrt(coop_sum(loc, part));
+  int sweeps = 0;
+  if (r0 != 0.0) {
+    const double target = 1e-12 * r0;
+    for (int sweep = 0; sweep < 400; ++sweep) {
+      for (int32_t cc = 0; cc < ncolors; ++cc) {
+        const int32_t i0 = cptr[cc], i1 = cptr[cc + 1];
+        for (int32_t hh = hptr[cc] + blockIdx.x; hh < hptr[cc + 1]; hh += gridDim.x) {
+          const int32_t i = heavy[hh];
+          const double dot = block_dot(pcol, pval, x, prp[i], prp[i + 1]);
+          if (threadIdx.x == 0) {
+            const int32_t u = row_ids[i];
+            x[u] = (b[u] - dot) / pdiag[i];
+          }
+        }
+        const int64_t span = ((int64_t)(i1 - i0) * G + 31) / 32 * 32;
+        for (int64_t t = gtid; t < span; t += gstride) {
+          const int64_t i = i0 + t / G;
+          const bool ok = i < i1 && prp[i + 1] - prp[i] <= kHeavyRow;
+          const double dot = group_dot<G, true>(pcol, pval, x, ok ? prp[i] : 0, ok ? prp[i + 1] : 0);
+          if (ok && (threadIdx.x & (G - 1)) == 0) {
+            const int32_t u = row_ids[i];
+            x[u] = (b[u] - dot) / pdiag[i];
+          }
+        }
+        cg::this_grid().sync();
+      }
+      loc = 0.0;
+      for (int64_t u = gtid; u < a.n; u += gstride) loc += x[u];
+      const double mean = coop_sum(loc, part) / (double)a.n;
+      for (int64_t u = gtid; u < a.n; u += gstride) x[u] = x[u] - mean;
+      cg::this_grid().sync();
+      coop_residual<G>(a, b, x, r, heavy_nat, nheavy_nat);
+      cg::this_grid().sync();
+      loc = 0.0;
+      for (int64_t u = gtid; u < a.n; u += gstride) loc += r[u] * r[u];
+      ++sweeps;
+      if (sqrt(coop_sum(loc, part)) <= target) break;
+    }
+  }
+  if (gtid == 0) *sweeps_out = sweeps;
+}
+
+int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const double* b, double* x, double* r) {
+  const int threads = 256;
+  const void* k = cl.group == 8 ? (const void*)relax_coop_kernel<8> : (const void*)relax_coop_kernel<1>;
+  const int blocks = c.max_coop_blocks(k, threads);
+  static thread_local DVec<double> part;
+  if (part.n < blocks || part.s != c.s) part.alloc(blocks, c.s);
+  int* sw = c.dflag + 30;
+  CSRv av = a;
+  const int64_t* prp = cl.rp.p;
+  const int32_t* pcol = cl.col.p;
+  const double* pval = cl.val.p;
+  const double* pdiag = cl.diag.p;
+  const int32_t* rid = cl.row_ids.p;
+  const int32_t* cptr = (const int32_t*)(cl.rp.p + a.n + 1);
+  int32_t nc = cl.ncolors;
+  double* pp = part.p;
+  const int32_t* hv = cl.heavy.p;
+  const int32_t* hp = cl.hptr.p;
+  const int32_t* hn = cl.heavy_nat.p;
+  int32_t nhn = cl.nheavy_nat;
+  void* args[] = {&av, (void*)&prp, (void*)&pcol, (void*)&pval, (void*)&pdiag, (void*)&rid, (void*)&cptr, &nc,
+                  (void*)&hv, (void*)&hp, (void*)&hn, &nhn, (void*)&b, &x, &r, &pp, &sw};
+  coop_launch(c, k, blocks, threads, args);
+  return read_i32(c, sw);
 }
 
 // Rows [0, cn) of the inverse of each bordered LU factor: x = Minv[:cn,:cn] b
