@@ -147,24 +147,24 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
   int32_t p_c[U];
   double p_v[U];
   auto prefetch = [&](int c) {
-    const int32_t c0 = cached ? s_cptr[c] : L.cptr[c];
-    const int32_t c1 = cached ? s_cptr[c + 1] : L.cptr[c + 1];
+    const int32_t c0 = cached ? s_cptr[c] : __ldg(L.cptr + c);
+    const int32_t c1 = cached ? s_cptr[c + 1] : __ldg(L.cptr + c + 1);
     const int64_t i = c0 + slot;
     p_ok = i < c1;
     p_k0 = p_k1 = 0;
     if (p_ok) {
-      p_u = L.row_ids[i];
-      p_k0 = L.prp[i];
-      p_k1 = L.prp[i + 1];
-      p_d = L.pdiag[i];
+      p_u = __ldg(L.row_ids + i);
+      p_k0 = __ldg(L.prp + i);
+      p_k1 = __ldg(L.prp + i + 1);
+      p_d = __ldg(L.pdiag + i);
       p_b = b[p_u];
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int64_t k = p_k0 + lane + (int64_t)j * G;
       const bool ok = k < p_k1;
-      p_c[j] = ok ? L.pcol[k] : 0;
-      p_v[j] = ok ? L.pval[k] : 0.0;
+      p_c[j] = ok ? __ldg(L.pcol + k) : 0;
+      p_v[j] = ok ? __ldg(L.pval + k) : 0.0;
     }
   };
   prefetch(0);
@@ -191,7 +191,7 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
           acc = 0.0;
 #pragma unroll
           for (int j = 0; j < U; ++j) acc += p_v[j] * xv[j];
-          for (int64_t k = p_k0 + lane + (int64_t)U * G; k < p_k1; k += G) acc += L.pval[k] * x[L.pcol[k]];
+          for (int64_t k = p_k0 + lane + (int64_t)U * G; k < p_k1; k += G) acc += __ldg(L.pval + k) * x[__ldg(L.pcol + k)];
 #pragma unroll
           for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
           if (p_ok && lane == 0) x[p_u] = (p_b - acc) / p_d;
@@ -237,21 +237,42 @@ __device__ inline void gs_group(const TLevel& L, const double* __restrict__ b, d
 }
 
 template <class S>
-__device__ inline void gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps, TailCounters* ctr) {
+__device__ inline void gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps, TailCounters* ctr,
+                          int32_t xs_rows) {
   __shared__ int32_t s_cptr[kMaxColors];
   if (L.ncolors == 0 || sweeps == 0) return;
-  if (S::leader()) ctr->phases += (long long)sweeps * L.ncolors;
-  if (!std::is_same<S, GridScope>::value && L.smem_ok) {
-    gs_smem(L, b, x, sweeps, ctr);
-    return;
-  }
   const long long tg = clock64();
-  if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps, s_cptr, ctr);
-  else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps, s_cptr, ctr);
-  else gs_group<S, 1>(L, b, x, sweeps, s_cptr, ctr);
+  if (S::leader()) ctr->phases += (long long)sweeps * L.ncolors;
+  constexpr bool cta = !std::is_same<S, GridScope>::value;
+  if (cta && L.smem_ok) {
+    gs_smem(L, b, x, sweeps, ctr);
+  } else if (cta && L.n <= xs_rows) {
+    // x and b of the level in shared memory for the sweeps: every gather of
+    // the dependent chain is an LDS; the matrix streams through L1
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* sx = (double*)smem;
+    double* sb = sx + L.n;
+    for (int32_t i = threadIdx.x; i < L.n; i += blockDim.x) {
+      sx[i] = x[i];
+      sb[i] = b[i];
+    }
+    __syncthreads();
+    if (L.group == 8) gs_group<S, 8>(L, sb, sx, sweeps, s_cptr, ctr);
+    else if (L.group == 4) gs_group<S, 4>(L, sb, sx, sweeps, s_cptr, ctr);
+    else gs_group<S, 1>(L, sb, sx, sweeps, s_cptr, ctr);
+    for (int32_t i = threadIdx.x; i < L.n; i += blockDim.x) x[i] = sx[i];
+    __syncthreads();
+  } else {
+    if (L.group == 8) gs_group<S, 8>(L, b, x, sweeps, s_cptr, ctr);
+    else if (L.group == 4) gs_group<S, 4>(L, b, x, sweeps, s_cptr, ctr);
+    else gs_group<S, 1>(L, b, x, sweeps, s_cptr, ctr);
+  }
   if (S::leader()) {
-    ctr->cyc_global_gs += clock64() - tg;
+    const long long dt = clock64() - tg;
+    ctr->cyc_global_gs += dt;
     ctr->global_phases += (long long)sweeps * L.ncolors;
+    ctr->lvl_gs_cyc[L.id] += dt;
+    ctr->lvl_gs_calls[L.id] += 1;
   }
 }
 
@@ -380,7 +401,7 @@ __device__ inline double scope_sum(double v, double* sh, double* part) {
 // RelaxationSolver::solve (coarse_solver.cpp:82-93)
 template <class S>
 __device__ inline void relax(const TLevel& L, const double* b, double* x, double* sh, double* part,
-                             TailCounters* ctr) {
+                             TailCounters* ctr, int32_t xs_rows) {
   residual<S>(L, b, x, L.r);
   double loc = 0.0;
   for (int64_t u = S::tid(); u < L.n; u += S::stride()) loc += L.r[u] * L.r[u];
@@ -389,7 +410,7 @@ __device__ inline void relax(const TLevel& L, const double* b, double* x, double
   if (r0 == 0.0) return;
   const double target = 1e-12 * r0;
   for (int sweep = 0; sweep < 400; ++sweep) {
-    gs<S>(L, b, x, 1, ctr);
+    gs<S>(L, b, x, 1, ctr, xs_rows);
     loc = 0.0;
     for (int64_t u = S::tid(); u < L.n; u += S::stride()) loc += x[u];
     const double mean = scope_sum<S>(loc, sh, part) / (double)L.n;
@@ -426,27 +447,28 @@ __device__ inline int take(double* credits, int l, double gamma) {
 
 template <class S>
 __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
-                           int32_t small_rows, double* sh, double* part, TailCounters* ctr);
+                           int32_t small_rows, double* sh, double* part, TailCounters* ctr, int32_t xs_rows);
 
 // CTA 0 runs a small subtree alone; the other CTAs wait at the grid barrier
 __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, double* credits, double mu,
-                                     int32_t small_rows, double* sh, double* part, TailCounters* ctr) {
+                                     int32_t small_rows, double* sh, double* part, TailCounters* ctr,
+                                     int32_t xs_rows) {
   if (levels[f.l].n > small_rows) return false;
-  if (blockIdx.x == 0) visit_loop<BlockScope>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr);
+  if (blockIdx.x == 0) visit_loop<BlockScope>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
   GridScope::sync();
   return true;
 }
 
 template <class S>
 __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
-                           int32_t small_rows, double* sh, double* part, TailCounters* ctr) {
+                           int32_t small_rows, double* sh, double* part, TailCounters* ctr, int32_t xs_rows) {
   Frame st[kMaxLevels];
   int sp = 0;
   st[sp++] = Frame{l0, theta0, 0, 0};
   while (sp > 0) {
     Frame& f = st[sp - 1];
     if (std::is_same<S, GridScope>::value && f.step == 0 && f.it == 0 &&
-        small_handoff(levels, f, credits, mu, small_rows, sh, part, ctr)) {
+        small_handoff(levels, f, credits, mu, small_rows, sh, part, ctr, xs_rows)) {
       --sp;
       continue;
     }
@@ -458,7 +480,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
       continue;
     }
     if (L.coarsest == CM_RELAX) {
-      relax<S>(L, L.b, L.x, sh, part, ctr);
+      relax<S>(L, L.b, L.x, sh, part, ctr, xs_rows);
       --sp;
       continue;
     }
@@ -469,7 +491,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
           --sp;
           continue;
         }
-        if (C.nu_pre) gs<S>(L, L.b, L.x, C.nu_pre, ctr);
+        if (C.nu_pre) gs<S>(L, L.b, L.x, C.nu_pre, ctr, xs_rows);
         residual<S>(L, L.b, L.x, L.r);
         restrict_to<S>(L, C, L.r, mu);
         if (S::leader()) ctr->work += (double)L.m * (C.nu_pre + 1);
@@ -478,7 +500,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
         st[sp++] = Frame{f.l + 1, th, 0, 0};
       } else {
         interpolate<S>(L, C, L.x);
-        if (C.nu_post) gs<S>(L, L.b, L.x, C.nu_post, ctr);
+        if (C.nu_post) gs<S>(L, L.b, L.x, C.nu_post, ctr, xs_rows);
         if (S::leader()) ctr->work += (double)L.m * C.nu_post;
         ++f.it;
         f.step = 0;
@@ -528,13 +550,14 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
 template <int MINB>
 __global__ void __launch_bounds__(kTailThreads, MINB) tail_kernel(const TLevel* __restrict__ levels, int nlevels, int l0,
                                                             int theta0, double* credits_g, double mu,
-                                                            int32_t small_rows, double* part, TailCounters* ctr) {
+                                                            int32_t small_rows, double* part, TailCounters* ctr,
+                                                            int32_t xs_rows) {
   __shared__ double credits[kMaxLevels];
   __shared__ double sh[64];
   const long long t_start = clock64();
   for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = credits_g[l];
   __syncthreads();
-  visit_loop<GridScope>(levels, l0, theta0, credits, mu, small_rows, sh, part, ctr);
+  visit_loop<GridScope>(levels, l0, theta0, credits, mu, small_rows, sh, part, ctr, xs_rows);
   if (blockIdx.x == 0) {
     for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits_g[l] = credits[l];
     if (threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
@@ -558,7 +581,11 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   const char* e1 = getenv("LAMG_TAIL_SMALL");
   small_rows = e1 ? atoi(e1) : 4096;
   const char* e3 = getenv("LAMG_TAIL_SMEM_KB");
-  smem = e3 ? std::min(kTailSmemMax, atoi(e3) * 1024) : 0;  // default: operators via L1/L2
+  smem = e3 ? std::min(kTailSmemMax, atoi(e3) * 1024) : 0;  // operators via L1/L2 unless set
+  // x and b of the CTA-scope levels in shared memory (LAMG_TAIL_XSMEM=1; measured
+  // neutral on cfg2: the phases are bound by the L2 chain of the operator rows)
+  const char* e5 = getenv("LAMG_TAIL_XSMEM");
+  xs_rows = (e5 && atoi(e5) == 1) ? small_rows : 0;
   const char* e2 = getenv("LAMG_TAIL_CTAS");
   ctas = std::max(1, std::min(e2 ? atoi(e2) : 8, 16));  // one cluster (<= 16 CTAs)
   std::vector<TLevel> tl(nl);
@@ -566,6 +593,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     const DLevel& L = *h.levels[l];
     TLevel& t = tl[l];
     memset(&t, 0, sizeof t);
+    t.id = l;
     const CSRv a = L.op.view();
     t.n = a.n;
     t.m = a.m;
@@ -623,6 +651,12 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
       }
     }
   }
+  xs_rows = std::min(xs_rows, small_rows);
+  smem = std::max(smem, (int)(2 * 8 * (int64_t)xs_rows));
+  if (smem > kTailSmemMax) {
+    xs_rows = 0;
+    smem = std::min(smem, kTailSmemMax);
+  }
   dlevels.alloc(nl, c.s);
   CK(cudaMemcpyAsync(dlevels.p, tl.data(), sizeof(TLevel) * nl, cudaMemcpyHostToDevice, c.s));
   credits.alloc(nl, c.s);
@@ -679,8 +713,9 @@ void TailPlan::run(Ctx& c, int l, int theta, double mu, int nlevels) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   count_launch();
-  if (occ2) CK(cudaLaunchKernelEx(&cfg, tail_kernel<2>, lv, nlevels, l, theta, cr, mu, sr, pt, ct));
-  else CK(cudaLaunchKernelEx(&cfg, tail_kernel<1>, lv, nlevels, l, theta, cr, mu, sr, pt, ct));
+  int32_t xr = xs_rows;
+  if (occ2) CK(cudaLaunchKernelEx(&cfg, tail_kernel<2>, lv, nlevels, l, theta, cr, mu, sr, pt, ct, xr));
+  else CK(cudaLaunchKernelEx(&cfg, tail_kernel<1>, lv, nlevels, l, theta, cr, mu, sr, pt, ct, xr));
 }
 
 void TailPlan::collect(Ctx& c, double* work, int* relax_sweeps) {
@@ -698,10 +733,19 @@ void TailPlan::collect(Ctx& c, double* work, int* relax_sweeps) {
             h.smem_calls ? (double)h.cyc_stage / h.smem_calls : 0.0,
             h.smem_phases ? (double)h.cyc_phases / h.smem_phases : 0.0, h.global_phases,
             h.global_phases ? (double)h.cyc_global_gs / h.global_phases : 0.0);
-  if (getenv("LAMG_TAIL_DEBUG") && h.global_phases)
+  if (getenv("LAMG_TAIL_DEBUG")) print_debug(h);
+}
+
+void TailPlan::print_debug(const TailCounters& h) const {
+  if (h.global_phases)
     fprintf(stderr, "[tail] grid phase breakdown (CTA0 thread0, cycles/phase): fold %.0f extra %.0f prefetch %.0f barrier %.0f\n",
             (double)h.ph_fold / h.global_phases, (double)h.ph_extra / h.global_phases,
             (double)h.ph_prefetch / h.global_phases, (double)h.ph_barrier / h.global_phases);
+  for (int l = 0; l < kMaxLevels; ++l)
+    if (h.lvl_gs_calls[l])
+      fprintf(stderr, "[tail]   level %2d: gs calls %8lld  %10.0f cycles/call  %5.1f%% of tail cycles\n", l,
+              h.lvl_gs_calls[l], (double)h.lvl_gs_cyc[l] / h.lvl_gs_calls[l],
+              100.0 * h.lvl_gs_cyc[l] / std::max(1LL, h.cyc_total));
 }
 
 }  // namespace lamgb

@@ -18,11 +18,13 @@ struct TailCounters {
   long long cyc_total, cyc_gs;
   long long smem_calls, smem_phases, cyc_stage, cyc_phases, cyc_global_gs, global_phases;
   long long ph_fold, ph_extra, ph_prefetch, ph_barrier;
+  long long lvl_gs_cyc[kMaxLevels], lvl_gs_calls[kMaxLevels];  // per level (CTA 0, thread 0)
 };
 
 // one level as the tail kernel sees it: operator (natural + colour-permuted),
 // the transfer to its child, and its workspace vectors
 struct TLevel {
+  int id;
   int32_t n;
   int64_t m;
   const int64_t* rp;
@@ -73,6 +75,7 @@ struct TailPlan {
   int32_t small_rows = 4096;  // levels this small run in CTA 0 alone
   int ctas = 64;
   int smem = kTailSmemMax;  // bytes of dynamic shared memory per tail CTA
+  int32_t xs_rows = 0;      // CTA-scope sweeps keep x and b of levels this small in shared memory
   bool occ2 = true;         // two tail CTAs per SM (64-register variant)
   const void* kernel = nullptr;
   DVec<TLevel> dlevels;
@@ -82,6 +85,7 @@ struct TailPlan {
   void build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows);
   void reset(Ctx& c);
   void run(Ctx& c, int l, int theta, double mu, int nlevels);
+  void print_debug(const TailCounters& h) const;
   void collect(Ctx& c, double* work, int* relax_sweeps);
 };
 
