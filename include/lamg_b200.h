@@ -160,6 +160,19 @@ int lamg_solve(lamg_ctx *ctx, const lamg_hier *h, const double *b, const double 
 int lamg_solve_dev(lamg_ctx *ctx, const lamg_hier *h, const double *d_b, const double *d_x0,
                    const lamg_cycle_cfg *cfg, double *d_x, lamg_solve_stats *stats,
                    double *residuals, int32_t residuals_cap);
+/* nrhs independent right-hand sides (cycle.cpp:221-273 per column; the
+ * reference runs one solve per RHS). b, x0, x are
+ * RHS-major [nrhs][n]; stats[nrhs]; residuals [nrhs][residuals_cap].
+ * THROUGHPUT mode + flat cycle: blocks of up to 32 columns share every
+ * kernel of the cycle (node-major n x K vectors on the device); each column
+ * is returned at the cycle its own convergence test fires. Otherwise: one
+ * solve per column (VALIDATE: each bit-identical to the reference). */
+int lamg_solve_batch(lamg_ctx *ctx, const lamg_hier *h, int32_t nrhs, const double *b,
+                     const double *x0, const lamg_cycle_cfg *cfg, double *x,
+                     lamg_solve_stats *stats, double *residuals, int32_t residuals_cap);
+int lamg_solve_batch_dev(lamg_ctx *ctx, const lamg_hier *h, int32_t nrhs, const double *d_b,
+                         const double *d_x0, const lamg_cycle_cfg *cfg, double *d_x,
+                         lamg_solve_stats *stats, double *residuals, int32_t residuals_cap);
 /* builds (once) the throughput-mode colour-permuted copies of the hierarchy */
 int lamg_hier_prepare_throughput(lamg_ctx *ctx, lamg_hier *h);
 

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 
+#include "batch.cuh"
 #include "solve.cuh"
 
 using namespace lamgb;
@@ -140,6 +141,86 @@ int solve_common(lamg_ctx* ctx, const lamg_hier* h, const double* b, const doubl
   return rc;
 }
 
+void fill_stats(const SolveResult& res, lamg_solve_stats* stats, double* residuals, int32_t cap) {
+  if (stats) {
+    stats->acf = res.acf;
+    stats->solve_work = res.solve_work;
+    stats->cycles = res.cycles;
+    stats->converged = res.converged ? 1 : 0;
+    stats->recombinations = res.recombinations;
+    stats->recomb_max_growth = res.recomb_max_growth;
+    stats->nresiduals = (int32_t)res.residuals.size();
+    stats->relax_sweeps = res.relax_sweeps;
+  }
+  if (residuals)
+    for (int32_t i = 0; i < cap && i < (int32_t)res.residuals.size(); ++i) residuals[i] = res.residuals[i];
+}
+
+// nrhs right-hand sides, RHS-major [nrhs][n]: blocks of <= 32 columns in
+// THROUGHPUT mode (batch.cuh), one reference-order solve per column otherwise
+int solve_batch_common(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const double* b, const double* x0, bool dev,
+                       const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
+                       int32_t cap) {
+  std::vector<SolveResult> all;
+  int status = LAMG_OK;
+  int rc = guarded([&] {
+    if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    if (nrhs < 0 || (nrhs > 0 && (!b || !x0 || !x))) throw LamgError(LAMG_E_ARGUMENT, "bad batch arguments");
+    Ctx& c = ctx->c;
+    set_device(c);
+    const int64_t n = h->h->levels[0]->op.n;
+    CycleCfg cc;
+    if (cfg) {
+      cc.correction = cfg->correction;
+      cc.mu = cfg->mu;
+      cc.max_cycles = cfg->max_cycles;
+      cc.target_reduction = cfg->target_reduction;
+      cc.divergence_factor = cfg->divergence_factor;
+    }
+    const bool blocked = c.mode == LAMG_MODE_THROUGHPUT && cc.correction == 0 && nrhs > 1;
+    const int chunk = blocked ? 32 : 1;
+    DVec<double> db, dx0, dx;
+    if (!dev) {
+      const int64_t w = std::min<int64_t>(nrhs, chunk) * n;
+      db.alloc(w, c.s);
+      dx0.alloc(w, c.s);
+      dx.alloc(w, c.s);
+    }
+    for (int32_t j0 = 0; j0 < nrhs; j0 += chunk) {
+      const int cnt = std::min<int32_t>(chunk, nrhs - j0);
+      const double* bj = dev ? b + j0 * n : db.p;
+      const double* xj0 = dev ? x0 + j0 * n : dx0.p;
+      double* xj = dev ? x + j0 * n : dx.p;
+      if (!dev) {
+        db.upload(b + j0 * n, cnt * n);
+        dx0.upload(x0 + j0 * n, cnt * n);
+      }
+      std::vector<SolveResult> part;
+      int r;
+      if (blocked) {
+        r = solve_batch_device(c, *h->h, cnt, bj, xj0, cc, xj, part);
+      } else {
+        part.resize(1);
+        r = solve_device(c, *h->h, bj, xj0, cc, xj, part[0]);
+      }
+      if (r != LAMG_OK && status == LAMG_OK) status = r;
+      if (!dev) {
+        dx.download(x + j0 * n, cnt * n);
+        c.sync();
+      }
+      for (auto& p : part) all.push_back(std::move(p));
+    }
+    if (status != LAMG_OK) {
+      for (auto& p : all)
+        if (!p.message.empty()) throw LamgError(status, p.message);
+      throw LamgError(status, "batched solve failed");
+    }
+  });
+  for (size_t j = 0; j < all.size(); ++j)
+    fill_stats(all[j], stats ? stats + j : nullptr, residuals ? residuals + (int64_t)j * cap : nullptr, cap);
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -172,6 +253,9 @@ int lamg_ctx_create(int device, int mode, lamg_ctx** out) {
     CK(cudaMalloc(&c.dflag, 64 * sizeof(int)));
     CK(cudaMalloc(&c.dscal, 256 * sizeof(double)));
     CK(cudaMalloc(&c.dpart, 256 * sizeof(double)));
+    CK(cudaMalloc(&c.dbpart, (size_t)32 * kColChunks * sizeof(double)));
+    CK(cudaMalloc(&c.dbscal, 256 * sizeof(double)));
+    CK(cudaMalloc(&c.dbdone, 64 * sizeof(int32_t)));
     c.clear_err();
     *out = x;
   });
@@ -191,6 +275,8 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   cudaStreamSynchronize(c.s);
   delete c.ws;
   c.ws = nullptr;
+  delete c.bws;
+  c.bws = nullptr;
   c.res_csr = DCSR();
   c.res_stage.f_diag.release();
   c.res_stage.f_ptr.release();
@@ -206,6 +292,9 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   cudaFree(c.dflag);
   cudaFree(c.dscal);
   cudaFree(c.dpart);
+  cudaFree(c.dbpart);
+  cudaFree(c.dbscal);
+  cudaFree(c.dbdone);
   cudaStreamDestroy(c.s);
   delete ctx;
 }
@@ -375,6 +464,18 @@ int lamg_solve(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double*
 int lamg_solve_dev(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, const lamg_cycle_cfg* cfg,
                    double* x, lamg_solve_stats* stats, double* residuals, int32_t cap) {
   return solve_common(ctx, h, b, x0, true, cfg, x, stats, residuals, cap);
+}
+
+int lamg_solve_batch(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const double* b, const double* x0,
+                     const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
+                     int32_t cap) {
+  return solve_batch_common(ctx, h, nrhs, b, x0, false, cfg, x, stats, residuals, cap);
+}
+
+int lamg_solve_batch_dev(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const double* b, const double* x0,
+                         const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
+                         int32_t cap) {
+  return solve_batch_common(ctx, h, nrhs, b, x0, true, cfg, x, stats, residuals, cap);
 }
 
 int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {

@@ -195,6 +195,10 @@ struct Ctx {
   double work = 0.0;            // thread-local work::total() equivalent (edge units)
   Profile prof;
   Workspace* ws = nullptr;      // solve workspace (owned; solve.cu)
+  Workspace* bws = nullptr;     // batched (K right-hand sides) solve workspace
+  double* dbpart = nullptr;     // batched reductions: per-column chunk partials (32 x kColChunks)
+  double* dbscal = nullptr;     // batched scalars (256 doubles)
+  int32_t* dbdone = nullptr;    // batched per-column masks (64 ints)
   // per-kernel API results kept until taken
   DCSR res_csr;
   struct {

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "batch.cuh"
 #include "solve.cuh"
 
 namespace lamgb {
@@ -49,9 +50,10 @@ void Workspace::clear_graphs() {
   graphs.clear();
 }
 
-void Workspace::ensure(Ctx& c, const DHier& h) {
-  if (owner == h.uid && lv.size() == h.levels.size()) return;
+void Workspace::ensure(Ctx& c, const DHier& h, int K_) {
+  if (owner == h.uid && lv.size() == h.levels.size() && K == K_) return;
   owner = h.uid;
+  K = K_;
   tail_built = false;
   clear_graphs();
   lv.clear();
@@ -60,7 +62,7 @@ void Workspace::ensure(Ctx& c, const DHier& h) {
   for (size_t l = 0; l < h.levels.size(); ++l) {
     const DLevel& L = *h.levels[l];
     LevelWS& w = lv[l];
-    const int32_t n = L.op.n;
+    const int64_t n = (int64_t)L.op.n * K;
     w.b.alloc(n, c.s);  // level 0: fixed-address copies of the solve's b and x (graph replay)
     w.x.alloc(n, c.s);
     w.r.alloc(n, c.s);
@@ -70,8 +72,8 @@ void Workspace::ensure(Ctx& c, const DHier& h) {
       w.stage_rhs.resize(st.size());
       w.stage_x.resize(st.size());
       for (size_t s = 1; s < st.size(); ++s) {
-        w.stage_rhs[s].alloc(st[s]->parent_n, c.s);
-        w.stage_x[s].alloc(st[s]->parent_n, c.s);
+        w.stage_rhs[s].alloc((int64_t)st[s]->parent_n * K, c.s);
+        w.stage_x[s].alloc((int64_t)st[s]->parent_n * K, c.s);
       }
     }
   }
@@ -226,6 +228,8 @@ struct Driver {
   double* growth;
   int64_t recombinations = 0;
   int relax_sweeps = 0;
+  int K = 1;                     // right-hand sides per block (batch.cuh)
+  std::vector<int> relax_cols;   // K > 1: relaxation sweeps per column
 
   void visit(size_t l, const double* b, double* x, int theta) {
     if (!exact && (int)l >= ws.tail.first) {
@@ -243,6 +247,18 @@ struct Driver {
 
   void coarsest(size_t l, const double* b, double* x) {
     const DLevel& L = *h.levels[l];
+    if (K > 1) {
+      if (L.coarsest == CM_DIRECT) {
+        bdirect(c, *L.direct, b, x, K);
+      } else {
+        if (!L.color) throw LamgError(LAMG_E_ERROR, "batched relaxation needs the coloured operator");
+        std::vector<int> sw;
+        brelax(c, L.op.view(), *L.color, b, x, ws.lv[l].r.p, K, sw);
+        relax_cols.resize(K, 0);
+        for (int k = 0; k < K; ++k) relax_cols[k] += sw[k];
+      }
+      return;
+    }
     if (L.coarsest == CM_DIRECT) {
       direct_solve(c, *L.direct, b, x, exact, ws.direct_scratch.p);
     } else {
@@ -262,7 +278,8 @@ struct Driver {
     const double* in = b;
     for (size_t s = 0; s < S; ++s) {
       double* out = s + 1 < S ? ws.lv[0].stage_rhs[s + 1].p : ws.lv[1].b.p;
-      coarsen_rhs(c, st[s]->view(), in, out);
+      if (K > 1) bcoarsen_rhs(c, st[s]->view(), in, out, K);
+      else coarsen_rhs(c, st[s]->view(), in, out);
       c.work += (double)st[s]->nnzf;
       in = out;
     }
@@ -283,7 +300,8 @@ struct Driver {
     for (size_t s = 0; s < S; ++s) {
       double* out = s + 1 < S ? w.stage_rhs[s + 1].p : wc.b.p;
       if (!cached) {
-        coarsen_rhs(c, st[s]->view(), rhs[s], out);
+        if (K > 1) bcoarsen_rhs(c, st[s]->view(), rhs[s], out, K);
+        else coarsen_rhs(c, st[s]->view(), rhs[s], out);
         c.work += (double)st[s]->nnzf;
       }
       if (s + 1 < S) rhs[s + 1] = out;
@@ -293,7 +311,8 @@ struct Driver {
       const double* cur = x;
       for (size_t s = 0; s < S; ++s) {
         double* out = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
-        inject(c, st[s]->view(), cur, out);
+        if (K > 1) binject(c, st[s]->view(), cur, out, K);
+        else inject(c, st[s]->view(), cur, out);
         cur = out;
       }
       int theta_child = credits.take(l + 1, child.gamma);
@@ -301,7 +320,8 @@ struct Driver {
       for (size_t s = S; s-- > 0;) {
         const double* xc = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
         double* out = s == 0 ? x : w.stage_x[s].p;
-        backsub(c, st[s]->view(), xc, rhs[s], out);
+        if (K > 1) bbacksub(c, st[s]->view(), xc, rhs[s], out, K);
+        else backsub(c, st[s]->view(), xc, rhs[s], out);
         c.work += (double)st[s]->nnzf;
       }
     }
@@ -311,18 +331,24 @@ struct Driver {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 0, true);
-    if (!exact && L.color) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
+    if (K > 1) {
+      if (!L.color) throw LamgError(LAMG_E_ERROR, "batched smoothing needs the coloured operator");
+      bgs_colored(c, *L.color, L.op.n, b, x, sweeps, K);
+    } else if (!exact && L.color) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
     else gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
-    if (p) prof_mark(c, 0, false, (24.0 * L.op.m + 40.0 * L.op.n + 8.0) * sweeps);
+    // algorithmic bytes: operator once (8(n+1) + 24m + 8n) + per column x
+    // read, b read, x write (24n); K = 1 gives SURVEY.md 8(d)'s 24m + 40n + 8
+    if (p) prof_mark(c, 0, false, (24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K) * sweeps);
     c.work += (double)L.op.m * sweeps;
   }
   void resid(size_t l, const double* b, const double* x, double* r) {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
-    if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
+    if (K > 1) bresidual(c, L.op.view(), L.color.get(), b, x, r, K);
+    else if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
     else residual_exact(c, L.op.view(), b, x, r, L.sched.heavy_nat.p, L.sched.nheavy_nat);
-    if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 40.0 * L.op.n + 8.0);
+    if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K);
     c.work += (double)L.op.m;
   }
 
@@ -344,11 +370,16 @@ struct Driver {
         copy_d(c, w.saved_r[nsaved].p, w.r.p, L.op.n);
         ++nsaved;
       }
-      restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p);
-      wc.x.zero();
+      if (K > 1) {
+        brestrict(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p, wc.x.p, K);
+      } else {
+        restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p);
+        wc.x.zero();
+      }
       int theta_child = credits.take(l + 1, child.gamma);
       visit(l + 1, wc.b.p, wc.x.p, theta_child);
-      interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
+      if (K > 1) binterpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x, K);
+      else interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
       if (child.nu_post) gs(l, b, x, child.nu_post);
     }
     if (adaptive && nsaved > 0) {
@@ -522,6 +553,173 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   res.recomb_max_growth = read_scalar(c, growth);
   res.relax_sweeps = d.relax_sweeps;
   return rc;
+}
+
+// ------------------------------------------------------- batched solve
+// cycle.cpp:221-273 for nrhs <= 32 right-hand sides at once (THROUGHPUT
+// mode). The visit sequence is data-independent (LevelCredit), so one cycle
+// schedule -- one CUDA graph per credit state -- serves every column; each
+// column is copied out at the cycle where its own test (r <= r0/1e10, or
+// divergence) fires, exactly the iterate a one-column solve returns.
+int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const double* X0, const CycleCfg& cfg,
+                       double* X, std::vector<SolveResult>& res) {
+  if (nrhs < 1 || nrhs > 32) throw LamgError(LAMG_E_ARGUMENT, "batched solve takes 1..32 right-hand sides");
+  if (c.mode != LAMG_MODE_THROUGHPUT || cfg.correction != 0)
+    throw LamgError(LAMG_E_ARGUMENT, "batched solve runs the flat THROUGHPUT cycle");
+  const DLevel& L0 = *h.levels[0];
+  const int64_t n = L0.op.n;
+  const int K = batch_width_for(nrhs);
+  res.assign(nrhs, SolveResult{});
+  if (!h.throughput_ready) {
+    prepare_throughput(c, const_cast<DHier&>(h));
+    const_cast<DHier&>(h).throughput_ready = true;
+  }
+  if (!c.bws) c.bws = new Workspace();
+  Workspace& ws = *c.bws;
+  ws.ensure(c, h, K);
+  ws.top_rhs_valid = false;
+  if (!ws.tail_built) {
+    const char* env = getenv("LAMG_BATCH_TAIL_ROWS");
+    ws.tail.build(c, h, ws, env ? atoi(env) : 40000);
+    ws.tail_built = true;
+  }
+  ws.tail.reset(c);
+  double* Xw = ws.lv[0].x.p;
+  double* Bw = ws.lv[0].b.p;
+  double* Rw = ws.lv[0].r.p;
+  to_node_major(c, B, n, nrhs, K, Bw);
+  to_node_major(c, X0, n, nrhs, K, Xw);
+  // compatibility per column: |sum b| <= 1e-10 ||b||_inf
+  unsigned long long* bmax = (unsigned long long*)c.dbscal;  // [K]
+  double* bsum = c.dbscal + 32;                              // [K]
+  double* rn_d = c.dbscal + 64;                              // [K]
+  double* xsum = c.dbscal + 96;                              // [K]
+  bcolabsmax(c, Bw, n, K, bmax);
+  bcolsum(c, Bw, n, K, false, bsum);
+  CK(cudaMemcpyAsync(c.hscal, c.dbscal, 64 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  for (int j = 0; j < nrhs; ++j) {
+    double b_inf;
+    memcpy(&b_inf, &c.hscal[j], sizeof b_inf);
+    const double b_sum = c.hscal[32 + j];
+    if (std::fabs(b_sum) > 1e-10 * b_inf)
+      throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
+  }
+  const double w0 = c.work = 0.0;
+  Driver d{c, h, cfg, ws, LevelCredits{}, false, c.dscal + 151};
+  d.K = K;
+  d.credits.credit.assign(h.levels.size(), 0.0);
+  CK(cudaMemsetAsync(c.dscal + 151, 0, sizeof(double), c.s));
+  std::vector<double> rn(K), r0(K), target(K);
+  auto read_norms = [&] {
+    CK(cudaMemcpyAsync(c.hscal, rn_d, K * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    for (int k = 0; k < K; ++k) rn[k] = std::sqrt(c.hscal[k]);
+  };
+  d.resid(0, Bw, Xw, Rw);
+  bcolsum(c, Rw, n, K, true, rn_d);
+  read_norms();
+  std::vector<char> done(nrhs, 0);
+  int active = nrhs;
+  bool any_zero = false;
+  for (int j = 0; j < nrhs; ++j) {
+    r0[j] = rn[j];
+    target[j] = r0[j] / cfg.target_reduction;
+    res[j].residuals.push_back(r0[j]);
+    if (r0[j] == 0.0) any_zero = true;
+  }
+  if (any_zero) {  // r0 == 0: the answer is x0 minus its mean (cycle.cpp:234-238)
+    bcolsum(c, Xw, n, K, false, xsum);
+    for (int j = 0; j < nrhs; ++j)
+      if (r0[j] == 0.0) {
+        column_out(c, Xw, n, K, j, X + j * n, xsum);
+        res[j].converged = true;
+        done[j] = 1;
+        --active;
+      }
+  }
+  const char* eg = getenv("LAMG_GRAPHS");
+  const bool use_graphs = (int)h.levels.size() - 1 >= ws.tail.first && !c.prof.enabled && !(eg && atoi(eg) == 0);
+  if (use_graphs) d.prepare_top(Bw);
+  std::vector<double> work_at(1, 0.0);
+  int cycle = 0;
+  for (cycle = 1; cycle <= cfg.max_cycles && active > 0; ++cycle) {
+    auto one_cycle = [&] {
+      d.visit(0, Bw, Xw, 1);
+      bcolsum(c, Xw, n, K, false, xsum);
+      bsub_mean(c, Xw, n, K, xsum);
+      d.resid(0, Bw, Xw, Rw);
+      bcolsum(c, Rw, n, K, true, rn_d);
+    };
+    if (use_graphs) {
+      Workspace::CycleGraph* g = nullptr;
+      for (auto& e : ws.graphs)
+        if (e.key == d.credits.credit) g = &e;
+      if (!g) {
+        Workspace::CycleGraph e;
+        e.key = d.credits.credit;
+        const double wc = c.work;
+        const long long l0 = t_launches;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+        one_cycle();
+        CK(cudaStreamEndCapture(c.s, &graph));
+        CK(cudaGraphInstantiate(&e.exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        e.work = c.work - wc;
+        e.launches = t_launches - l0;
+        g_launches -= e.launches;
+        t_launches = l0;
+        e.credits_after = d.credits.credit;
+        c.work = wc;
+        ws.graphs.push_back(std::move(e));
+        g = &ws.graphs.back();
+      }
+      CK(cudaGraphLaunch(g->exec, c.s));
+      g_launches += g->launches;
+      c.work += g->work;
+      d.credits.credit = g->credits_after;
+    } else {
+      one_cycle();
+    }
+    work_at.push_back(c.work);
+    read_norms();
+    for (int j = 0; j < nrhs; ++j) {
+      if (done[j]) continue;
+      res[j].residuals.push_back(rn[j]);
+      res[j].cycles = cycle;
+      if (rn[j] <= target[j]) {
+        res[j].converged = true;
+      } else if (rn[j] > cfg.divergence_factor * r0[j] || !std::isfinite(rn[j])) {
+        res[j].message = "solve diverged: residual grew from " + to_string_f(r0[j]) + " to " + to_string_f(rn[j]);
+      } else {
+        continue;
+      }
+      column_out(c, Xw, n, K, j, X + j * n);
+      done[j] = 1;
+      --active;
+    }
+  }
+  for (int j = 0; j < nrhs; ++j)
+    if (!done[j]) column_out(c, Xw, n, K, j, X + j * n);  // max_cycles reached
+  // the on-device tail's work is read once at the end; cycles are identical in
+  // structure, so a column's share is proportional to its cycle count
+  double tail_work = 0.0;
+  int tail_relax = 0;
+  ws.tail.collect(c, &tail_work, &tail_relax);
+  const int ran = std::max(1, cycle - 1);
+  for (int j = 0; j < nrhs; ++j) {
+    SolveResult& r = res[j];
+    const int cj = r.cycles;
+    const double wj = work_at[std::min<size_t>(cj, work_at.size() - 1)] - w0 + tail_work * cj / ran;
+    r.solve_work = wj / (double)L0.op.m;
+    r.acf = cj > 0 && r0[j] > 0.0 ? std::pow(r.residuals.back() / r0[j], 1.0 / cj) : 0.0;
+    r.relax_sweeps = (j < (int)d.relax_cols.size() ? d.relax_cols[j] : 0) + tail_relax;
+  }
+  c.sync();
+  for (int j = 0; j < nrhs; ++j)
+    if (!res[j].message.empty()) return LAMG_E_DIVERGED;
+  return LAMG_OK;
 }
 
 }  // namespace lamgb

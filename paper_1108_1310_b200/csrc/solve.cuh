@@ -45,6 +45,7 @@ struct LevelWS {
 // per-context solve workspace, sized for the last hierarchy solved
 struct Workspace {
   uint64_t owner = 0;  // DHier::uid
+  int K = 1;           // right-hand sides per block: every vector is n x K, node-major
   std::vector<LevelWS> lv;
   DVec<double> direct_scratch;
   bool top_rhs_valid = false;
@@ -61,7 +62,7 @@ struct Workspace {
   std::vector<CycleGraph> graphs;
   void clear_graphs();
   ~Workspace() { clear_graphs(); }
-  void ensure(Ctx& c, const DHier& h);
+  void ensure(Ctx& c, const DHier& h, int K = 1);
   void ensure_adaptive(Ctx& c, const DHier& h);
 };
 
@@ -71,5 +72,11 @@ void recombine_api(Ctx& c, const CSRv& a, const double* b, int cols, LevelWS& w,
 
 int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
                  double* x, SolveResult& res);
+
+// THROUGHPUT mode, K right-hand sides in one block (batch.cuh). B and X0 are
+// device RHS-major [nrhs][n]; X (device, RHS-major) receives every column at
+// the cycle it converged (or stopped); res[j] are the per-column stats.
+int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const double* X0, const CycleCfg& cfg,
+                       double* X, std::vector<SolveResult>& res);
 
 }  // namespace lamgb

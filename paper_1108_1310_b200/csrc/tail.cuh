@@ -19,6 +19,7 @@ struct TailCounters {
   long long smem_calls, smem_phases, cyc_stage, cyc_phases, cyc_global_gs, global_phases;
   long long ph_fold, ph_extra, ph_prefetch, ph_barrier;
   long long lvl_gs_cyc[kMaxLevels], lvl_gs_calls[kMaxLevels];  // per level (CTA 0, thread 0)
+  long long lvl_ph[kMaxLevels][4];  // batched sweeps: first row, extra rows, prefetch, barrier
 };
 
 // one level as the tail kernel sees it: operator (natural + colour-permuted),
@@ -41,6 +42,7 @@ struct TLevel {
   const double* pdiag;
   int group;    // lanes per row (1, 4, 8)
   int smem_ok;  // the coloured operator + x + b fit the tail CTA's shared memory
+  int smem_cs;  // K > 1: the operator + this CTA's column slice of x and b fit
   // workspace
   double* b;
   double* x;
@@ -77,6 +79,9 @@ struct TailPlan {
   int smem = kTailSmemMax;  // bytes of dynamic shared memory per tail CTA
   int32_t xs_rows = 0;      // CTA-scope sweeps keep x and b of levels this small in shared memory
   bool occ2 = true;         // two tail CTAs per SM (64-register variant)
+  int K = 1;                // right-hand sides per block (batch.cuh)
+  int threads = 512;        // per tail CTA
+  bool subtree = false;     // K > 1: plain launch, one column slice per CTA, CTA scope only
   const void* kernel = nullptr;
   DVec<TLevel> dlevels;
   DVec<double> credits;

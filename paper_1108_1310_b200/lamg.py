@@ -357,6 +357,35 @@ def solve(h: Hierarchy, b, x0, cfg: CycleConfig | None = None, ctx: Context | No
     return x, stats
 
 
+def solve_batch(h: Hierarchy, B, X0, cfg: CycleConfig | None = None, ctx: Context | None = None):
+    """nrhs independent solves (one lamg::solve per row of B, cycle.cpp:221-273).
+
+    B and X0 are [nrhs, n]. THROUGHPUT mode runs blocks of up to 32 columns
+    through one cycle schedule (lamg_solve_batch); VALIDATE mode solves each
+    column in the reference's order. Returns (X [nrhs, n], [SolveStats]).
+    """
+    ctx = ctx or h.ctx
+    cfg = cfg or CycleConfig()
+    B, X0 = np.ascontiguousarray(B, dtype=np.float64), np.ascontiguousarray(X0, dtype=np.float64)
+    if B.ndim != 2 or B.shape != X0.shape or B.shape[1] != h.n:
+        raise DimensionMismatchError("solve_batch: B and X0 must be [nrhs, n] with n the finest size")
+    nrhs = B.shape[0]
+    X = np.empty_like(B)
+    st = (_lib.lamg_solve_stats * max(nrhs, 1))()
+    cap = cfg.max_cycles + 2
+    res = np.empty((max(nrhs, 1), cap))
+    c = cfg.c()
+    code = ctx.lib.lamg_solve_batch(ctx.p, h.h, C.c_int32(nrhs), _p(B), _p(X0), C.byref(c), _p(X), st, _p(res),
+                                    C.c_int32(cap))
+    stats = [SolveStats(list(res[j, :min(st[j].nresiduals, cap)]), st[j].acf, st[j].solve_work, st[j].cycles,
+                        bool(st[j].converged), st[j].recombinations, st[j].recomb_max_growth, st[j].relax_sweeps)
+             for j in range(nrhs)]
+    if code == 7:
+        raise DivergedError(_lib.lib().lamg_last_error().decode(), [s.as_dict() for s in stats])
+    _check(code)
+    return X, stats
+
+
 def level_cycle_index(h: Hierarchy, l: int, gamma: float) -> float:
     return h.level_cycle_index(l, gamma)
 
