@@ -432,203 +432,26 @@ __device__ inline void relax(const TLevel& L, const double* b, double* x, double
 
 
 // ------------------------------------------------- K right-hand sides
-// (batch.cuh): thread t of the scope owns column k = t % K of row t / K; the
-// scope stride is a multiple of K, so a thread keeps its column throughout.
-// Coloured sweep over K columns. The K lanes of a group load their row's
-// entries cooperatively (entry q*K + lane), the fold broadcasts them with
-// shuffles, so the x gathers of a row are all in flight at once. The first
-// row of each group's next phase (row id, extent, diagonal, rhs, up to 4K
-// entries) is loaded before the barrier; after it only the gathers remain.
-template <class S, int K>
-__device__ inline void bgs_t(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
-                             const int32_t* done, TailCounters* ctr) {
-  if (L.ncolors == 0 || sweeps == 0) return;
-  constexpr int Q = 4;
-  const long long tg = clock64();
-  const int lane = (int)(S::tid() % K);
-  const int64_t slot = S::tid() / K;
-  const bool frozen = done && done[lane];
-  bool p_ok = false;
-  int32_t p_u = 0;
-  int64_t p_k0 = 0, p_k1 = 0;
-  double p_d = 1.0, p_b = 0.0;
-  int32_t p_c[Q];
-  double p_v[Q];
-  auto prefetch = [&](int cc) {
-    const int32_t c0 = __ldg(L.cptr + cc), c1 = __ldg(L.cptr + cc + 1);
-    const int64_t i = c0 + slot;
-    p_ok = i < c1;
-    p_k0 = p_k1 = 0;
-    if (p_ok) {
-      p_u = __ldg(L.row_ids + i);
-      p_k0 = __ldg(L.prp + i);
-      p_k1 = __ldg(L.prp + i + 1);
-      p_d = __ldg(L.pdiag + i);
-      p_b = b[(int64_t)p_u * K + lane];
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int64_t e = p_k0 + q * K + lane;
-      p_c[q] = e < p_k1 ? __ldg(L.pcol + e) : 0;
-      p_v[q] = e < p_k1 ? __ldg(L.pval + e) : 0.0;
-    }
-  };
-  const int64_t warp_slot0 = (S::tid() & ~31ll) / K;  // first row slot of this warp
-  auto warp_active = [&](int cc) { return warp_slot0 < (int64_t)(__ldg(L.cptr + cc + 1) - __ldg(L.cptr + cc)); };
-  if (warp_active(0)) prefetch(0);
-  long long acc[4] = {0, 0, 0, 0};
-  for (int sw = 0; sw < sweeps; ++sw)
-    for (int32_t cc = 0; cc < L.ncolors; ++cc) {
-      const long long tA = clock64();
-      const int32_t i0 = __ldg(L.cptr + cc), i1 = __ldg(L.cptr + cc + 1);
-      if (warp_slot0 < (int64_t)(i1 - i0)) {  // the prefetched row
-        const int len = (int)(p_k1 - p_k0);
-        const int maxlen = __reduce_max_sync(0xffffffffu, len);
-        double s = p_b;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          if (q * K >= maxlen) break;
-          constexpr int JB = K < 8 ? K : 8;  // entries gathered per round
-#pragma unroll
-          for (int j0 = 0; j0 < K; j0 += JB) {
-            if (q * K + j0 >= maxlen) break;
-            double xv[JB], vv[JB];
-#pragma unroll
-            for (int j = 0; j < JB; ++j) {
-              const int c = __shfl_sync(0xffffffffu, p_c[q], j0 + j, K);
-              vv[j] = __shfl_sync(0xffffffffu, p_v[q], j0 + j, K);
-              xv[j] = q * K + j0 + j < len ? x[(int64_t)c * K + lane] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < JB; ++j)
-              if (q * K + j0 + j < len) s = s - vv[j] * xv[j];
-          }
-        }
-        if (len > Q * K) s = col_fold<K, true>(s, L.pcol, L.pval, x, p_k0 + Q * K, p_k1, lane);
-        if (p_ok && !frozen) x[(int64_t)p_u * K + lane] = s / p_d;
-      }
-      const long long tB = clock64();
-      // rows beyond the first slot of this colour (large colours only)
-      if (!frozen)
-        for (int64_t t = S::tid() + S::stride(); t < (int64_t)(i1 - i0) * K; t += S::stride()) {
-          const int64_t i = i0 + t / K;
-          const int32_t u = __ldg(L.row_ids + i);
-          const double s = col_fold<K, true, 16>(b[(int64_t)u * K + lane], L.pcol, L.pval, x, __ldg(L.prp + i),
-                                             __ldg(L.prp + i + 1), lane);
-          x[(int64_t)u * K + lane] = s / __ldg(L.pdiag + i);
-        }
-      const long long tC = clock64();
-      const int next = cc + 1 < L.ncolors ? cc + 1 : (sw + 1 < sweeps ? 0 : -1);
-      if (next >= 0 && warp_active(next)) prefetch(next);
-      else p_ok = false, p_k0 = p_k1 = 0;
-      const long long tD = clock64();
-      S::sync();
-      acc[0] += tB - tA;
-      acc[1] += tC - tB;
-      acc[2] += tD - tC;
-      acc[3] += clock64() - tD;
-    }
-  if (S::leader()) {
-    for (int q = 0; q < 4; ++q) ctr->lvl_ph[L.id][q] += acc[q];
-    ctr->phases += (long long)sweeps * L.ncolors;
-    ctr->lvl_gs_cyc[L.id] += clock64() - tg;
-    ctr->lvl_gs_calls[L.id] += 1;
-  }
-}
-
-template <class S, int K>
-__device__ inline void bresidual_t(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
-  for (int64_t t = S::tid(); t < (int64_t)L.n * K; t += S::stride()) {
-    const int64_t u = t / K;
-    const int k = (int)(t % K);
-    const double s = col_fold<K, false, 16>(__ldg(L.diag + u) * x[t], L.col, L.val, x, __ldg(L.rp + u),
-                                        __ldg(L.rp + u + 1), k);
-    r[t] = b[t] - s;
-  }
-  S::sync();
-}
-
-template <class S, int K>
-__device__ inline void brestrict_t(const TLevel& L, const TLevel& C, const double* r, double mu) {
-  for (int64_t t = S::tid(); t < (int64_t)C.n * K; t += S::stride()) {
-    const int64_t g = t / K;
-    const int k = (int)(t % K);
-    double s = 0.0;
-    for (int64_t j = L.mem_ptr[g]; j < L.mem_ptr[g + 1]; ++j) s = s + r[(int64_t)L.mem[j] * K + k];
-    C.b[t] = mu != 1.0 ? s * mu : s;
-    C.x[t] = 0.0;
-  }
-  S::sync();
-}
-
-template <class S, int K>
-__device__ inline void binterp_t(const TLevel& L, const TLevel& C, double* x) {
-  for (int64_t t = S::tid(); t < (int64_t)L.n * K; t += S::stride())
-    x[t] = x[t] + C.x[(int64_t)L.agg[t / K] * K + (t % K)];
-  S::sync();
-}
-
-template <class S, int K>
-__device__ inline void bcoarsen_t(const StageV& s, const double* b, double* bc) {
-  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * K; t += S::stride()) {
-    const int64_t q = t / K;
-    const int k = (int)(t % K);
-    double v = b[(int64_t)s.poc[q] * K + k];
-    for (int64_t j = s.t_ptr[q]; j < s.t_ptr[q + 1]; ++j) {
-      const int64_t p = s.t_p[j];
-      const int32_t i = s.f_of_p[p];
-      v = v - s.f_val[p] * (b[(int64_t)s.f_nodes[i] * K + k] / s.f_diag[i]);
-    }
-    bc[t] = v;
-  }
-  S::sync();
-}
-
-template <class S, int K>
-__device__ inline void binject_t(const StageV& s, const double* x, double* xc) {
-  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * K; t += S::stride())
-    xc[t] = x[(int64_t)s.poc[t / K] * K + (t % K)];
-  S::sync();
-}
-
-template <class S, int K>
-__device__ inline void bbacksub_t(const StageV& s, const double* xc, const double* b, double* x) {
-  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * K; t += S::stride())
-    x[(int64_t)s.poc[t / K] * K + (t % K)] = xc[t];
-  S::sync();
-  for (int64_t t = S::tid(); t < (int64_t)s.nf * K; t += S::stride()) {
-    const int64_t i = t / K;
-    const int k = (int)(t % K);
-    const int32_t f = s.f_nodes[i];
-    double sum = b[(int64_t)f * K + k];
-    for (int64_t p = s.f_ptr[i]; p < s.f_ptr[i + 1]; ++p) sum = sum - s.f_val[p] * x[(int64_t)s.f_nbr[p] * K + k];
-    x[(int64_t)f * K + k] = sum / s.f_diag[i];
-  }
-  S::sync();
-}
-
-// ---- column slices: below small_rows every CTA of the cluster runs the
-// sub-cycle alone on its own columns [k0, k0+kc) of the K-wide block (the
-// columns are independent systems with one visit sequence), so a phase is a
-// __syncthreads and the operator rows stay in the CTA's L1 (no cluster
-// barrier, hence no L1 invalidation, inside the subtree).
+// (batch.cuh). Below the host-driven levels, a block of K columns runs as K/kc
+// independent CTAs (subtree_kernel): each CTA runs the whole sub-cycle for
+// its own kc columns, so a phase is a __syncthreads, and it never waits on
+// another CTA. Inside the subtree every vector is COLUMN-major, v[k*n + u]:
+// the CTAs' writes never share a cache sector (node-major rows would put all
+// K columns of a node in one 256-byte segment written by K different SMs).
+// The subtree's root level is transposed in at entry and out at exit.
 struct ColSlice {
-  int k0, kc;
+  int k0, kc, sh;  // kc = 1 << sh columns starting at k0
 };
-template <class S, int K>
+template <int K>
 __device__ inline ColSlice my_cols() {
-  if constexpr (std::is_same<S, GridScope>::value) {
-    return ColSlice{0, K};
-  } else {
-    const int kc = K >= (int)gridDim.x ? K / (int)gridDim.x : 1;
-    return ColSlice{(int)blockIdx.x * kc, kc};
-  }
+  const int kc = K >= (int)gridDim.x ? K / (int)gridDim.x : 1;  // powers of two
+  return ColSlice{(int)blockIdx.x * kc, kc, __ffs(kc) - 1};
 }
 
-// CTA-scope column-slice forms (K > 1). The sweep keeps each thread's
-// first (row, column) pair of the next colour -- row id, extent, diagonal,
-// rhs and up to kCU entries -- in registers, loaded before the barrier; after
-// it the x gathers of the row are issued together and folded in entry order.
+// Coloured sweep, column slice. The first (row, column) pair of each
+// thread's next colour -- row id, extent, diagonal, rhs and up to kCU
+// entries -- is loaded before the barrier; after it only the x gathers of
+// the row remain, issued together and folded in entry order.
 constexpr int kCU = 16;
 template <int K>
 __device__ inline void cs_gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
@@ -636,15 +459,23 @@ __device__ inline void cs_gs(const TLevel& L, const double* __restrict__ b, doub
   __shared__ int32_t s_cp[kMaxColors + 1];
   if (L.ncolors == 0 || sweeps == 0) return;
   const long long tg = clock64();
-  const ColSlice sl = my_cols<BlockScope, K>();
+  const ColSlice sl = my_cols<K>();
   const int nc = L.ncolors;
+  const int64_t n = L.n;
   const bool cached = nc <= kMaxColors;
   if (cached)
     for (int i = threadIdx.x; i <= nc; i += blockDim.x) s_cp[i] = __ldg(L.cptr + i);
   __syncthreads();
-  const int k = sl.k0 + (int)(threadIdx.x % sl.kc);
+  const int k = sl.k0 + (int)(threadIdx.x & (sl.kc - 1));
+  const double* bk = b + k * n;
+  double* xk = x + k * n;
   const bool frozen = done && done[k];
-  const int64_t slot = threadIdx.x / sl.kc;
+  const int64_t slot = threadIdx.x >> sl.sh;
+  const int64_t warp_t0 = threadIdx.x & ~31u;
+  auto cbounds = [&](int cc, int32_t& c0, int32_t& c1) {
+    c0 = cached ? s_cp[cc] : __ldg(L.cptr + cc);
+    c1 = cached ? s_cp[cc + 1] : __ldg(L.cptr + cc + 1);
+  };
   bool p_ok = false;
   int32_t p_u = 0;
   int64_t p_e0 = 0, p_e1 = 0;
@@ -652,16 +483,19 @@ __device__ inline void cs_gs(const TLevel& L, const double* __restrict__ b, doub
   int32_t p_c[kCU];
   double p_v[kCU];
   auto prefetch = [&](int cc) {
-    const int32_t c0 = cached ? s_cp[cc] : __ldg(L.cptr + cc), c1 = cached ? s_cp[cc + 1] : __ldg(L.cptr + cc + 1);
+    int32_t c0, c1;
+    cbounds(cc, c0, c1);
+    p_ok = false;
+    p_e0 = p_e1 = 0;
+    if (warp_t0 >= (int64_t)(c1 - c0) << sl.sh) return;  // whole warp idle in this colour
     const int64_t i = c0 + slot;
     p_ok = i < c1;
-    p_e0 = p_e1 = 0;
     if (p_ok) {
       p_u = __ldg(L.row_ids + i);
       p_e0 = __ldg(L.prp + i);
       p_e1 = __ldg(L.prp + i + 1);
       p_d = __ldg(L.pdiag + i);
-      p_b = b[(int64_t)p_u * K + k];
+      p_b = bk[p_u];
     }
 #pragma unroll
     for (int j = 0; j < kCU; ++j) {
@@ -670,38 +504,31 @@ __device__ inline void cs_gs(const TLevel& L, const double* __restrict__ b, doub
       p_v[j] = ok ? __ldg(L.pval + p_e0 + j) : 0.0;
     }
   };
-  // warps whose first pair lies beyond a colour skip its body (only the
-  // barrier): on small levels most of the CTA is idle in every phase
-  const int64_t warp_t0 = threadIdx.x & ~31u;
-  auto warp_active = [&](int cc) {
-    const int32_t c0 = cached ? s_cp[cc] : __ldg(L.cptr + cc), c1 = cached ? s_cp[cc + 1] : __ldg(L.cptr + cc + 1);
-    return warp_t0 < (int64_t)(c1 - c0) * sl.kc;
-  };
-  if (warp_active(0)) prefetch(0);
+  prefetch(0);
   for (int sw = 0; sw < sweeps; ++sw)
     for (int32_t cc = 0; cc < nc; ++cc) {
-      const int32_t i0 = cached ? s_cp[cc] : __ldg(L.cptr + cc), i1 = cached ? s_cp[cc + 1] : __ldg(L.cptr + cc + 1);
+      int32_t i0, i1;
+      cbounds(cc, i0, i1);
       if (p_ok && !frozen) {
         double xv[kCU];
 #pragma unroll
-        for (int j = 0; j < kCU; ++j) xv[j] = p_e0 + j < p_e1 ? x[(int64_t)p_c[j] * K + k] : 0.0;
+        for (int j = 0; j < kCU; ++j) xv[j] = p_e0 + j < p_e1 ? xk[p_c[j]] : 0.0;
         double s = p_b;
 #pragma unroll
         for (int j = 0; j < kCU; ++j)
           if (p_e0 + j < p_e1) s = s - p_v[j] * xv[j];
-        if (p_e1 - p_e0 > kCU) s = col_fold<K, true>(s, L.pcol, L.pval, x, p_e0 + kCU, p_e1, k);
-        x[(int64_t)p_u * K + k] = s / p_d;
+        if (p_e1 - p_e0 > kCU) s = col_fold<1, true, 8>(s, L.pcol, L.pval, xk, p_e0 + kCU, p_e1, 0);
+        xk[p_u] = s / p_d;
       }
       if (!frozen)  // pairs beyond the first of this colour (large colours only)
-        for (int64_t t = threadIdx.x + blockDim.x; t < (int64_t)(i1 - i0) * sl.kc; t += blockDim.x) {
-          const int64_t i = i0 + t / sl.kc;
+        for (int64_t t = threadIdx.x + blockDim.x; t < (int64_t)(i1 - i0) << sl.sh; t += blockDim.x) {
+          const int64_t i = i0 + (t >> sl.sh);
           const int32_t u = __ldg(L.row_ids + i);
-          const double s = col_fold<K, true, 16>(b[(int64_t)u * K + k], L.pcol, L.pval, x, __ldg(L.prp + i),
-                                                __ldg(L.prp + i + 1), k);
-          x[(int64_t)u * K + k] = s / __ldg(L.pdiag + i);
+          const double s = col_fold<1, true, 8>(bk[u], L.pcol, L.pval, xk, __ldg(L.prp + i), __ldg(L.prp + i + 1), 0);
+          xk[u] = s / __ldg(L.pdiag + i);
         }
       const int next = cc + 1 < nc ? cc + 1 : (sw + 1 < sweeps ? 0 : -1);
-      if (next >= 0 && warp_active(next)) prefetch(next);
+      if (next >= 0) prefetch(next);
       else p_ok = false;
       __syncthreads();
     }
@@ -723,12 +550,12 @@ __device__ inline void cs_gs_smem(const TLevel& L, const double* __restrict__ b,
                                   TailCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const long long tg = clock64();
-  const ColSlice sl = my_cols<BlockScope, K>();
+  const ColSlice sl = my_cols<K>();
   const int kc = sl.kc;
   const int32_t n = L.n;
   const int64_t nnz = 2 * L.m;
   const int nc = L.ncolors;
-  double* s_x = (double*)smem;
+  double* s_x = (double*)smem;  // [kc][n]
   double* s_b = s_x + (int64_t)n * kc;
   double* s_d = s_b + (int64_t)n * kc;
   double* s_v = s_d + n;
@@ -748,40 +575,38 @@ __device__ inline void cs_gs_smem(const TLevel& L, const double* __restrict__ b,
     s_c[e] = __ldg(L.pcol + e_base + e);
     s_v[e] = __ldg(L.pval + e_base + e);
   }
-  for (int64_t t = threadIdx.x; t < (int64_t)n * kc; t += blockDim.x) {
-    const int64_t u = t / kc;
-    const int64_t q = u * K + sl.k0 + t % kc;
-    s_x[t] = x[q];
-    s_b[t] = b[q];
+  for (int64_t t = threadIdx.x; t < (int64_t)n * kc; t += blockDim.x) {  // my columns are contiguous
+    s_x[t] = x[(int64_t)sl.k0 * n + t];
+    s_b[t] = b[(int64_t)sl.k0 * n + t];
   }
   __syncthreads();
   for (int sw = 0; sw < sweeps; ++sw)
     for (int cc = 0; cc < nc; ++cc) {
       const int32_t i0 = s_cp[cc], i1 = s_cp[cc + 1];
       for (int32_t t = threadIdx.x; t < (i1 - i0) * kc; t += blockDim.x) {
-        const int32_t i = i0 + t / kc;
-        const int j = t % kc;
+        const int32_t i = i0 + (t >> sl.sh);
+        const int j = t & (kc - 1);
+        const double* sxj = s_x + (int64_t)j * n;
         const int32_t u = s_id[i];
-        double s = s_b[u * kc + j];
+        double s = s_b[(int64_t)j * n + u];
         const int32_t e1 = s_rp[i + 1];
-        for (int32_t e0 = s_rp[i]; e0 < e1; e0 += 16) {  // loads of 16 entries ahead of their fold
-          double xv[16], vv[16];
+        for (int32_t e0 = s_rp[i]; e0 < e1; e0 += 8) {  // loads of 8 entries ahead of their fold
+          double xv[8], vv[8];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const bool ok = e0 + q < e1;
             vv[q] = ok ? s_v[e0 + q] : 0.0;
-            xv[q] = ok ? s_x[s_c[e0 + q] * kc + j] : 0.0;
+            xv[q] = ok ? sxj[s_c[e0 + q]] : 0.0;
           }
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
+          for (int q = 0; q < 8; ++q)
             if (e0 + q < e1) s = s - vv[q] * xv[q];
         }
-        s_x[u * kc + j] = s / s_d[i];
+        s_x[(int64_t)j * n + u] = s / s_d[i];
       }
       __syncthreads();
     }
-  for (int64_t t = threadIdx.x; t < (int64_t)n * kc; t += blockDim.x)
-    x[(t / kc) * K + sl.k0 + t % kc] = s_x[t];
+  for (int64_t t = threadIdx.x; t < (int64_t)n * kc; t += blockDim.x) x[(int64_t)sl.k0 * n + t] = s_x[t];
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctr->phases += (long long)sweeps * nc;
@@ -794,149 +619,152 @@ __device__ inline void cs_gs_smem(const TLevel& L, const double* __restrict__ b,
 
 template <int K>
 __device__ inline void cs_residual(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)L.n * sl.kc; t += blockDim.x) {
-    const int64_t u = t / sl.kc;
-    const int64_t q = u * K + sl.k0 + t % sl.kc;
-    const double s = col_fold<K, false, 16>(__ldg(L.diag + u) * x[q], L.col, L.val, x, __ldg(L.rp + u),
-                                        __ldg(L.rp + u + 1), (int)(q % K));
-    r[q] = b[q] - s;
+  const ColSlice sl = my_cols<K>();
+  const int64_t n = L.n;
+  for (int64_t t = threadIdx.x; t < n << sl.sh; t += blockDim.x) {
+    const int64_t u = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    const double* xk = x + k * n;
+    const double s = col_fold<1, false, 16>(__ldg(L.diag + u) * xk[u], L.col, L.val, xk, __ldg(L.rp + u),
+                                            __ldg(L.rp + u + 1), 0);
+    r[k * n + u] = b[k * n + u] - s;
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_restrict(const TLevel& L, const TLevel& C, const double* r, double mu) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)C.n * sl.kc; t += blockDim.x) {
-    const int64_t g = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
+  const ColSlice sl = my_cols<K>();
+  for (int64_t t = threadIdx.x; t < (int64_t)C.n << sl.sh; t += blockDim.x) {
+    const int64_t g = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    const double* rk = r + k * L.n;
     double s = 0.0;
-    for (int64_t j = __ldg(L.mem_ptr + g); j < __ldg(L.mem_ptr + g + 1); ++j) s = s + r[(int64_t)__ldg(L.mem + j) * K + k];
-    C.b[g * K + k] = mu != 1.0 ? s * mu : s;
-    C.x[g * K + k] = 0.0;
+    for (int64_t j = __ldg(L.mem_ptr + g); j < __ldg(L.mem_ptr + g + 1); ++j) s = s + rk[__ldg(L.mem + j)];
+    C.b[k * C.n + g] = mu != 1.0 ? s * mu : s;
+    C.x[k * C.n + g] = 0.0;
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_interp(const TLevel& L, const TLevel& C, double* x) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)L.n * sl.kc; t += blockDim.x) {
-    const int64_t u = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
-    x[u * K + k] = x[u * K + k] + C.x[(int64_t)__ldg(L.agg + u) * K + k];
+  const ColSlice sl = my_cols<K>();
+  for (int64_t t = threadIdx.x; t < (int64_t)L.n << sl.sh; t += blockDim.x) {
+    const int64_t u = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    x[k * L.n + u] = x[k * L.n + u] + C.x[k * C.n + __ldg(L.agg + u)];
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_coarsen(const StageV& s, const double* b, double* bc) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n * sl.kc; t += blockDim.x) {
-    const int64_t q = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
-    double v = b[(int64_t)__ldg(s.poc + q) * K + k];
+  const ColSlice sl = my_cols<K>();
+  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n << sl.sh; t += blockDim.x) {
+    const int64_t q = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    const double* bk = b + k * s.parent_n;
+    double v = bk[__ldg(s.poc + q)];
     for (int64_t j = __ldg(s.t_ptr + q); j < __ldg(s.t_ptr + q + 1); ++j) {
       const int64_t p = __ldg(s.t_p + j);
       const int32_t i = __ldg(s.f_of_p + p);
-      v = v - __ldg(s.f_val + p) * (b[(int64_t)__ldg(s.f_nodes + i) * K + k] / __ldg(s.f_diag + i));
+      v = v - __ldg(s.f_val + p) * (bk[__ldg(s.f_nodes + i)] / __ldg(s.f_diag + i));
     }
-    bc[q * K + k] = v;
+    bc[k * s.coarse_n + q] = v;
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_inject(const StageV& s, const double* x, double* xc) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n * sl.kc; t += blockDim.x) {
-    const int64_t q = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
-    xc[q * K + k] = x[(int64_t)__ldg(s.poc + q) * K + k];
+  const ColSlice sl = my_cols<K>();
+  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n << sl.sh; t += blockDim.x) {
+    const int64_t q = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    xc[k * s.coarse_n + q] = x[k * s.parent_n + __ldg(s.poc + q)];
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_backsub(const StageV& s, const double* xc, const double* b, double* x) {
-  const ColSlice sl = my_cols<BlockScope, K>();
-  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n * sl.kc; t += blockDim.x) {
-    const int64_t q = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
-    x[(int64_t)__ldg(s.poc + q) * K + k] = xc[q * K + k];
+  const ColSlice sl = my_cols<K>();
+  for (int64_t t = threadIdx.x; t < (int64_t)s.coarse_n << sl.sh; t += blockDim.x) {
+    const int64_t q = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    x[k * s.parent_n + __ldg(s.poc + q)] = xc[k * s.coarse_n + q];
   }
   __syncthreads();
-  for (int64_t t = threadIdx.x; t < (int64_t)s.nf * sl.kc; t += blockDim.x) {
-    const int64_t i = t / sl.kc;
-    const int k = sl.k0 + (int)(t % sl.kc);
+  for (int64_t t = threadIdx.x; t < (int64_t)s.nf << sl.sh; t += blockDim.x) {
+    const int64_t i = t >> sl.sh;
+    const int64_t k = sl.k0 + (t & (sl.kc - 1));
+    double* xk = x + k * s.parent_n;
     const int32_t f = __ldg(s.f_nodes + i);
-    double sum = b[(int64_t)f * K + k];
+    double sum = b[k * s.parent_n + f];
     for (int64_t p = __ldg(s.f_ptr + i); p < __ldg(s.f_ptr + i + 1); ++p)
-      sum = sum - __ldg(s.f_val + p) * x[(int64_t)__ldg(s.f_nbr + p) * K + k];
-    x[(int64_t)f * K + k] = sum / __ldg(s.f_diag + i);
+      sum = sum - __ldg(s.f_val + p) * xk[__ldg(s.f_nbr + p)];
+    xk[f] = sum / __ldg(s.f_diag + i);
   }
   __syncthreads();
 }
 
 template <int K>
 __device__ inline void cs_direct(const TLevel& L, const double* b, double* x) {
-  const ColSlice sl = my_cols<BlockScope, K>();
+  const ColSlice sl = my_cols<K>();
+  const int64_t n = L.n;
   for (int32_t ci = 0; ci < L.ncomp; ++ci) {
     const int32_t s0 = L.comp_start[ci], cn = L.comp_start[ci + 1] - s0;
     const double* Mi = L.inv + L.inv_off[ci];
-    for (int64_t t = threadIdx.x; t < (int64_t)cn * sl.kc; t += blockDim.x) {
-      const int32_t i = (int32_t)(t / sl.kc);
-      const int k = sl.k0 + (int)(t % sl.kc);
+    for (int64_t t = threadIdx.x; t < (int64_t)cn << sl.sh; t += blockDim.x) {
+      const int32_t i = (int32_t)(t >> sl.sh);
+      const int64_t k = sl.k0 + (t & (sl.kc - 1));
+      const double* bk = b + k * n;
       double s = 0.0;
-      for (int32_t j = 0; j < cn; ++j)
-        s += __ldg(Mi + (int64_t)i * cn + j) * b[(int64_t)(L.whole ? j : L.nodes[s0 + j]) * K + k];
-      x[(int64_t)(L.whole ? i : L.nodes[s0 + i]) * K + k] = s;
+      for (int32_t j = 0; j < cn; ++j) s += __ldg(Mi + (int64_t)i * cn + j) * bk[L.whole ? j : L.nodes[s0 + j]];
+      x[k * n + (L.whole ? i : L.nodes[s0 + i])] = s;
     }
     __syncthreads();
   }
 }
 
-// per-column sums in a K-independent order (chunks of R rows folded in
-// sequence, chunk sums folded in sequence); part holds [K][kChunks]
+// per-column sums of column-major X[k*n + u] in a K-independent order
+// (chunks of R rows folded in sequence, chunk sums folded in sequence);
+// part holds [K][kChunks]
 constexpr int kChunks = 256;
-template <class S, int K, bool SQ>
-__device__ inline double chunk_colsum(const double* X, int64_t n, double* part, ColSlice sl, int k) {
+template <bool SQ>
+__device__ inline double chunk_colsum(const double* X, int64_t n, double* part, ColSlice sl, int64_t k) {
   const int64_t R = (n + kChunks - 1) / kChunks;
   const int np = (int)((n + R - 1) / R);
-  for (int64_t t = S::tid(); t < (int64_t)np * sl.kc; t += S::stride()) {
-    const int64_t p = t / sl.kc;
-    const int kk = sl.k0 + (int)(t % sl.kc);
+  for (int64_t t = threadIdx.x; t < (int64_t)np << sl.sh; t += blockDim.x) {
+    const int64_t p = t >> sl.sh;
+    const int64_t kk = sl.k0 + (t & (sl.kc - 1));
     const int64_t u1 = (p + 1) * R < n ? (p + 1) * R : n;
     double s = 0.0;
     for (int64_t u = p * R; u < u1; ++u) {
-      const double v = X[u * K + kk];
+      const double v = X[kk * n + u];
       s += SQ ? v * v : v;
     }
-    part[(int64_t)kk * kChunks + p] = s;
+    part[kk * kChunks + p] = s;
   }
-  S::sync();
+  __syncthreads();
   double tot = 0.0;
-  for (int p = 0; p < np; ++p) tot += ((volatile double*)part)[(int64_t)k * kChunks + p];
-  S::sync();
+  for (int p = 0; p < np; ++p) tot += part[k * kChunks + p];
+  __syncthreads();
   return tot;
 }
 
-// RelaxationSolver::solve (coarse_solver.cpp:82-93) per column over the
-// scope's columns; each column freezes at its own tolerance
-template <class S, int K>
-__device__ inline void brelax_t(const TLevel& L, const double* b, double* x, double* part, TailCounters* ctr) {
+// RelaxationSolver::solve (coarse_solver.cpp:82-93) per column of the
+// slice; each column freezes at its own tolerance
+template <int K>
+__device__ inline void cs_relax(const TLevel& L, const double* b, double* x, double* part, TailCounters* ctr) {
   __shared__ int32_t bdone[32];
   __shared__ double br0[32];
-  constexpr bool grid = std::is_same<S, GridScope>::value;
-  const ColSlice sl = my_cols<S, K>();
-  const int k = sl.k0 + (int)(S::tid() % sl.kc);  // this thread's column (stride is a multiple of kc)
-  auto resid = [&] {
-    if constexpr (grid) bresidual_t<S, K>(L, b, x, L.r);
-    else cs_residual<K>(L, b, x, L.r);
-  };
-  resid();
-  const double r0 = sqrt(chunk_colsum<S, K, true>(L.r, L.n, part, sl, k));
+  const ColSlice sl = my_cols<K>();
+  const int64_t n = L.n;
+  const int64_t k = sl.k0 + (threadIdx.x & (sl.kc - 1));  // this thread's column
+  cs_residual<K>(L, b, x, L.r);
+  const double r0 = sqrt(chunk_colsum<true>(L.r, n, part, sl, k));
   if (threadIdx.x < 32) bdone[threadIdx.x] = 1;
   __syncthreads();
   if ((int)threadIdx.x < sl.kc) {
@@ -944,87 +772,76 @@ __device__ inline void brelax_t(const TLevel& L, const double* b, double* x, dou
     bdone[k] = r0 == 0.0;
   }
   __syncthreads();
-  if (S::leader()) ctr->work += (double)L.m;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->work += (double)L.m;
   for (int sweep = 0; sweep < 400; ++sweep) {
     int active = 0;
     for (int j = 0; j < sl.kc; ++j) active += !bdone[sl.k0 + j];
     if (!active) break;
-    if constexpr (grid) bgs_t<S, K>(L, b, x, 1, bdone, ctr);
-    else cs_gs<K>(L, b, x, 1, bdone, ctr);
-    const double mean = chunk_colsum<S, K, false>(x, L.n, part, sl, k) / (double)L.n;
+    cs_gs<K>(L, b, x, 1, bdone, ctr);
+    const double mean = chunk_colsum<false>(x, n, part, sl, k) / (double)n;
     if (!bdone[k])
-      for (int64_t t = S::tid(); t < (int64_t)L.n * sl.kc; t += S::stride()) {
-        const int64_t q = (t / sl.kc) * K + k;
-        x[q] = x[q] - mean;
-      }
-    S::sync();
-    resid();
-    const double rn = sqrt(chunk_colsum<S, K, true>(L.r, L.n, part, sl, k));
-    if (S::leader()) {
+      for (int64_t t = threadIdx.x; t < n << sl.sh; t += blockDim.x) x[k * n + (t >> sl.sh)] -= mean;
+    __syncthreads();
+    cs_residual<K>(L, b, x, L.r);
+    const double rn = sqrt(chunk_colsum<true>(L.r, n, part, sl, k));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctr->work += 2.0 * (double)L.m;
       ctr->relax_sweeps += 1;
     }
-    __syncthreads();
     if ((int)threadIdx.x < sl.kc && !bdone[k] && rn <= 1e-12 * br0[k]) bdone[k] = 1;
-    S::sync();
+    __syncthreads();
   }
 }
 
-// single-column, K-column grid, or K-column CTA-slice form of each operation
+// single-column (any scope) or K-column column-slice (CTA scope) form of each
+// operation of the recursion
 template <class S, int K>
 __device__ inline void op_gs(const TLevel& L, const double* b, double* x, int sweeps, TailCounters* ctr,
                              int32_t xs_rows) {
   if constexpr (K == 1) gs<S>(L, b, x, sweeps, ctr, xs_rows);
-  else if constexpr (std::is_same<S, GridScope>::value) bgs_t<S, K>(L, b, x, sweeps, nullptr, ctr);
   else if (L.smem_cs) cs_gs_smem<K>(L, b, x, sweeps, ctr);
   else cs_gs<K>(L, b, x, sweeps, nullptr, ctr);
 }
 template <class S, int K>
 __device__ inline void op_residual(const TLevel& L, const double* b, const double* x, double* r) {
   if constexpr (K == 1) residual<S>(L, b, x, r);
-  else if constexpr (std::is_same<S, GridScope>::value) bresidual_t<S, K>(L, b, x, r);
   else cs_residual<K>(L, b, x, r);
 }
 template <class S, int K>
 __device__ inline void op_restrict(const TLevel& L, const TLevel& C, const double* r, double mu) {
   if constexpr (K == 1) restrict_to<S>(L, C, r, mu);
-  else if constexpr (std::is_same<S, GridScope>::value) brestrict_t<S, K>(L, C, r, mu);
   else cs_restrict<K>(L, C, r, mu);
 }
 template <class S, int K>
 __device__ inline void op_interp(const TLevel& L, const TLevel& C, double* x) {
   if constexpr (K == 1) interpolate<S>(L, C, x);
-  else if constexpr (std::is_same<S, GridScope>::value) binterp_t<S, K>(L, C, x);
   else cs_interp<K>(L, C, x);
 }
 template <class S, int K>
 __device__ inline void op_coarsen(const StageV& s, const double* b, double* bc) {
   if constexpr (K == 1) coarsen<S>(s, b, bc);
-  else if constexpr (std::is_same<S, GridScope>::value) bcoarsen_t<S, K>(s, b, bc);
   else cs_coarsen<K>(s, b, bc);
 }
 template <class S, int K>
 __device__ inline void op_inject(const StageV& s, const double* x, double* xc) {
   if constexpr (K == 1) inject<S>(s, x, xc);
-  else if constexpr (std::is_same<S, GridScope>::value) binject_t<S, K>(s, x, xc);
   else cs_inject<K>(s, x, xc);
 }
 template <class S, int K>
 __device__ inline void op_backsub(const StageV& s, const double* xc, const double* b, double* x) {
   if constexpr (K == 1) backsub<S>(s, xc, b, x);
-  else if constexpr (std::is_same<S, GridScope>::value) bbacksub_t<S, K>(s, xc, b, x);
   else cs_backsub<K>(s, xc, b, x);
 }
 template <class S, int K>
 __device__ inline void op_direct(const TLevel& L, const double* b, double* x) {
   if constexpr (K == 1) direct(L, b, x);
-  else cs_direct<K>(L, b, x);  // the direct coarsest always runs in CTA scope
+  else cs_direct<K>(L, b, x);
 }
 template <class S, int K>
 __device__ inline void op_relax(const TLevel& L, const double* b, double* x, double* sh, double* part,
                                 TailCounters* ctr, int32_t xs_rows) {
   if constexpr (K == 1) relax<S>(L, b, x, sh, part, ctr, xs_rows);
-  else brelax_t<S, K>(L, b, x, part, ctr);
+  else cs_relax<K>(L, b, x, part, ctr);
 }
 
 struct Frame {
@@ -1054,9 +871,7 @@ __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, doubl
                                      int32_t small_rows, double* sh, double* part, TailCounters* ctr,
                                      int32_t xs_rows) {
   if (levels[f.l].n > small_rows) return false;
-  // K == 1: CTA 0 alone; K > 1: every CTA that owns columns, on its slice
-  if (K == 1 ? blockIdx.x == 0 : (int)blockIdx.x * (K >= (int)gridDim.x ? K / (int)gridDim.x : 1) < K)
-    visit_loop<BlockScope, K>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
+  if (blockIdx.x == 0) visit_loop<BlockScope, K>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
   GridScope::sync();
   return true;
 }
@@ -1064,6 +879,7 @@ __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, doubl
 template <class S, int K>
 __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
                            int32_t small_rows, double* sh, double* part, TailCounters* ctr, int32_t xs_rows) {
+  static_assert(K == 1 || std::is_same<S, BlockScope>::value, "K-column blocks run in CTA scope only");
   Frame st[kMaxLevels];
   int sp = 0;
   st[sp++] = Frame{l0, theta0, 0, 0};
@@ -1177,8 +993,21 @@ __global__ void __launch_bounds__(kTailThreadsBatch, 1) subtree_kernel(const TLe
   __shared__ double sh[64];
   const long long t_start = clock64();
   for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = credits_g[l];
+  // the root level arrives node-major from the host-driven levels: my columns in
+  const TLevel& R = levels[l0];
+  const ColSlice sl = my_cols<K>();
+  const int64_t n = R.n;
+  for (int64_t t = threadIdx.x; t < n << sl.sh; t += blockDim.x) {
+    const int64_t u = t >> sl.sh, k = sl.k0 + (t & (sl.kc - 1));
+    R.b[k * n + u] = R.nm_b[u * K + k];
+    R.x[k * n + u] = R.nm_x[u * K + k];
+  }
   __syncthreads();
   visit_loop<BlockScope, K>(levels, l0, theta0, credits, mu, small_rows, sh, part, ctr, xs_rows);
+  for (int64_t t = threadIdx.x; t < n << sl.sh; t += blockDim.x) {
+    const int64_t u = t >> sl.sh, k = sl.k0 + (t & (sl.kc - 1));
+    R.nm_x[u * K + k] = R.x[k * n + u];
+  }
   if (blockIdx.x == 0) {
     for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits_g[l] = credits[l];
     if (threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
@@ -1303,13 +1132,13 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     case 1: kernel = occ2 ? (const void*)tail_kernel<2, 1> : (const void*)tail_kernel<1, 1>; break;
     // K > 1: 256 threads (255 registers) -- the column-slice phases are
     // latency-bound chains, more warps per CTA only add issue overhead
-    case 4: kernel = subtree ? (const void*)subtree_kernel<4> : (const void*)tail_kernel<1, 4, kTailThreadsBatch>; break;
-    case 8: kernel = subtree ? (const void*)subtree_kernel<8> : (const void*)tail_kernel<1, 8, kTailThreadsBatch>; break;
+    case 4: kernel = (const void*)subtree_kernel<4>; break;
+    case 8: kernel = (const void*)subtree_kernel<8>; break;
     case 16:
-      kernel = subtree ? (const void*)subtree_kernel<16> : (const void*)tail_kernel<1, 16, kTailThreadsBatch>;
+      kernel = (const void*)subtree_kernel<16>;
       break;
     case 32:
-      kernel = subtree ? (const void*)subtree_kernel<32> : (const void*)tail_kernel<1, 32, kTailThreadsBatch>;
+      kernel = (const void*)subtree_kernel<32>;
       break;
     default: throw LamgError(LAMG_E_ARGUMENT, "tail: unsupported batch width");
   }
@@ -1341,6 +1170,15 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
       tl[l].smem_cs = L.color && L.op.n <= small_rows &&
                       cs_smem_bytes(L.op.n, 2 * L.op.m, L.color->ncolors, kc) <= smem;
     }
+  }
+  if (subtree) {  // column-major copies of the root level's b and x (see subtree_kernel)
+    const int64_t rn = (int64_t)h.levels[first]->op.n * K;
+    root_b.alloc(rn, c.s);
+    root_x.alloc(rn, c.s);
+    tl[first].nm_b = tl[first].b;
+    tl[first].nm_x = tl[first].x;
+    tl[first].b = root_b.p;
+    tl[first].x = root_x.p;
   }
   dlevels.alloc(nl, c.s);
   CK(cudaMemcpyAsync(dlevels.p, tl.data(), sizeof(TLevel) * nl, cudaMemcpyHostToDevice, c.s));

@@ -47,6 +47,8 @@ struct TLevel {
   double* b;
   double* x;
   double* r;
+  double* nm_b;  // subtree root (K > 1): the host's node-major b and x
+  double* nm_x;
   // solve parameters the parent uses when visiting this level
   double gamma;
   int nu_pre, nu_post;
@@ -86,6 +88,7 @@ struct TailPlan {
   DVec<TLevel> dlevels;
   DVec<double> credits;
   DVec<double> part;
+  DVec<double> root_b, root_x;  // K > 1: column-major root vectors
   DVec<TailCounters> ctr;
   void build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows);
   void reset(Ctx& c);
