@@ -2,12 +2,14 @@
 """Benchmark of the B200 LAMG hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lamg|reference]
-                    [--mode throughput|validate] [--config 2]
+                    [--mode throughput|validate] [--config 2] [--lanes 4] [--block 32]
 
-A step is one full LAMG solve (to the reference's relative residual 1e-10)
-of BASELINE.json config 2 -- the 3D 7-point 128^3 Laplacian with seeded
-log-uniform weights -- over a hierarchy built once on the GPU (setup is
-timed separately and reported). `value` is fine-level edges*cycles/s of the
+A step solves lanes x block right-hand sides (default 4 x 32), each to the
+reference's relative residual 1e-10, on BASELINE.json config 2 -- the 3D
+7-point 128^3 Laplacian with seeded log-uniform weights -- over a hierarchy
+built once on the GPU (setup is timed separately and reported). Each lane is
+one lamg_solve_batch_dev call on its own stream; the single-RHS solve time is
+reported beside it. `value` is fine-level edges*cycles/s of the
 whole job (sum over ranks of m1 * cycles per step / max-over-ranks device
 time), inputs resident in HBM; `e2e` is the same metric through the public
 C-ABI call with host buffers (H2D of b and x0, D2H of x and the residual
@@ -119,41 +121,68 @@ def sha(a) -> str:
 
 # ------------------------------------------------------------------- lamg
 class Lane:
-    """One concurrent solve lane: its own context (CUDA stream + workspace),
-    right-hand side and initial guess, over the shared device hierarchy."""
+    """One concurrent solve lane: its own context (CUDA stream + workspace)
+    over the shared device hierarchy, holding a block of k right-hand sides
+    (k = 1: lamg_solve_dev / lamg::solve; k > 1: lamg_solve_batch_dev /
+    lamg_solve_batch, RHS-major [k][n] buffers)."""
 
-    def __init__(self, L, torch, dev, h, mode, b, x0):
+    def __init__(self, L, torch, dev, h, mode, B, X0):
+        B, X0 = np.atleast_2d(B), np.atleast_2d(X0)
+        self.k = B.shape[0]
         self.ctx = L.Context(dev, mode)
         lib = self.ctx.lib
         lib.lamg_ctx_stream.restype = C.c_void_p
         self.stream = torch.cuda.ExternalStream(lib.lamg_ctx_stream(self.ctx.p), device=dev)
         self.h, self.L, self.lib = h, L, lib
-        self.db = torch.from_numpy(b).to(f"cuda:{dev}")
-        self.dx0 = torch.from_numpy(x0).to(f"cuda:{dev}")
+        self.db = torch.from_numpy(np.ascontiguousarray(B)).to(f"cuda:{dev}")
+        self.dx0 = torch.from_numpy(np.ascontiguousarray(X0)).to(f"cuda:{dev}")
         self.dx = torch.empty_like(self.db)
-        self.hb = torch.from_numpy(b).pin_memory().numpy()
-        self.hx0 = torch.from_numpy(x0).pin_memory().numpy()
+        self.hb = torch.from_numpy(np.ascontiguousarray(B)).pin_memory()
+        self.hx0 = torch.from_numpy(np.ascontiguousarray(X0)).pin_memory()
+        self.hx = torch.empty_like(self.hb).pin_memory()
         self.cfg = L.CycleConfig().c()
-        self.st = L._lib.lamg_solve_stats()
-        self.res = np.empty(512)
-        self.cycles = 0
+        self.st = (L._lib.lamg_solve_stats * self.k)()
+        self.cap = 512
+        self.res = np.empty(self.k * self.cap)
+        self.cycles = [0] * self.k
         self.err = None
+
+    def _ptr(self, t):
+        return C.c_void_p(t.data_ptr())
+
+    def _done(self, code):
+        self.L._check(code)
+        self.cycles = [int(self.st[j].cycles) for j in range(self.k)]
 
     def solve_dev(self):
         try:
-            code = self.lib.lamg_solve_dev(self.ctx.p, self.h.h, C.c_void_p(self.db.data_ptr()),
-                                           C.c_void_p(self.dx0.data_ptr()), C.byref(self.cfg),
-                                           C.c_void_p(self.dx.data_ptr()), C.byref(self.st),
-                                           self.res.ctypes.data_as(C.c_void_p), C.c_int32(512))
-            self.L._check(code)
-            self.cycles = self.st.cycles
+            if self.k == 1:
+                code = self.lib.lamg_solve_dev(self.ctx.p, self.h.h, self._ptr(self.db), self._ptr(self.dx0),
+                                               C.byref(self.cfg), self._ptr(self.dx), self.st,
+                                               self.res.ctypes.data_as(C.c_void_p), C.c_int32(self.cap))
+            else:
+                code = self.lib.lamg_solve_batch_dev(self.ctx.p, self.h.h, C.c_int32(self.k), self._ptr(self.db),
+                                                     self._ptr(self.dx0), C.byref(self.cfg), self._ptr(self.dx),
+                                                     self.st, self.res.ctypes.data_as(C.c_void_p),
+                                                     C.c_int32(self.cap))
+            self._done(code)
         except Exception as e:  # surfaced by the caller
             self.err = e
 
     def solve_host(self):
+        """The public host-buffer call: H2D of b and x0, D2H of x and the
+        residual histories happen inside it."""
         try:
-            self.x, so = self.L.solve(self.h, self.hb, self.hx0, self.L.CycleConfig(), ctx=self.ctx)
-            self.cycles = so.cycles
+            if self.k == 1:
+                code = self.lib.lamg_solve(self.ctx.p, self.h.h, self._ptr(self.hb), self._ptr(self.hx0),
+                                           C.byref(self.cfg), self._ptr(self.hx), self.st,
+                                           self.res.ctypes.data_as(C.c_void_p), C.c_int32(self.cap))
+            else:
+                code = self.lib.lamg_solve_batch(self.ctx.p, self.h.h, C.c_int32(self.k), self._ptr(self.hb),
+                                                 self._ptr(self.hx0), C.byref(self.cfg), self._ptr(self.hx),
+                                                 self.st, self.res.ctypes.data_as(C.c_void_p), C.c_int32(self.cap))
+            self._done(code)
+            self.x = self.hx.numpy()[0]
         except Exception as e:
             self.err = e
 
@@ -179,22 +208,41 @@ def run_lanes(lanes, fn, torch, stream0):
         e.record(ln.stream)
         ends.append(e)
     torch.cuda.synchronize()
-    return max(start.elapsed_time(e) for e in ends), [ln.cycles for ln in lanes]
+    return max(start.elapsed_time(e) for e in ends), [c for ln in lanes for c in ln.cycles]
+
+
+def kernel_profile(lib, lane, fn, ms_total):
+    """CUDA-event times of the finest-level GS / residual launches of one
+    profiled solve on `lane` (lamg_ctx_profile; graphs off while profiling)."""
+    lib.lamg_ctx_profile(lane.ctx.p, 1)
+    fn(lane)
+    kern = {}
+    for k, name in ((0, "gs_finest"), (1, "residual_finest")):
+        nl, tm, by = C.c_int64(), C.c_double(), C.c_double()
+        lib.lamg_ctx_profile_read(lane.ctx.p, C.c_int(k), C.byref(nl), C.byref(tm), C.byref(by))
+        if nl.value:
+            avg = tm.value / nl.value
+            kern[name] = {"launches": nl.value, "avg_ms": avg, "bytes": by.value,
+                          "gbs": by.value / (avg / 1e3) / 1e9, "total_ms": tm.value}
+    lib.lamg_ctx_profile(lane.ctx.p, 0)
+    return kern
 
 
 def run_lamg(args, dist: Dist):
     import torch
+    from paper_1108_1310_b200 import graphs as G
     from paper_1108_1310_b200 import lamg as L
 
     dev = dist.local
     torch.cuda.set_device(dev)
-    S = args.streams
+    NL, KB = args.lanes, args.block
     t0 = time.time()
     a, b, x0 = build_inputs(args.config, dist.rank)
-    from paper_1108_1310_b200 import graphs as G
-    rhs = [(b, x0)] + [(G.gaussian_rhs(a.n, 100 + args.config + 1000 * dist.rank + 7 * i),
-                        G.default_x0(a.n, seed=1 + dist.rank + 97 * i)) for i in range(1, S)]
-    log(f"[rank {dist.rank}] inputs n={a.n} m={a.m} ({S} right-hand sides) built in {time.time() - t0:.1f}s")
+    nrhs = NL * KB
+    B = np.stack([b] + [G.gaussian_rhs(a.n, 100 + args.config + 1000 * dist.rank + 7 * i) for i in range(1, nrhs)])
+    X0 = np.stack([x0] + [G.default_x0(a.n, seed=1 + dist.rank + 97 * i) for i in range(1, nrhs)])
+    log(f"[rank {dist.rank}] inputs n={a.n} m={a.m} ({NL} lanes x {KB} right-hand sides) built in "
+        f"{time.time() - t0:.1f}s")
     mode = L.MODE_THROUGHPUT if args.mode == "throughput" else L.MODE_VALIDATE
     ctx0 = L.Context(dev, mode)
     lib = ctx0.lib
@@ -206,32 +254,36 @@ def run_lamg(args, dist: Dist):
     if mode == L.MODE_THROUGHPUT:
         L._check(lib.lamg_hier_prepare_throughput(ctx0.p, h.h))
     log(f"[rank {dist.rank}] setup {setup_s:.2f}s, {h.nlevels} levels")
-    lanes = [Lane(L, torch, dev, h, mode, bb, xx) for bb, xx in rhs]
+    lanes = [Lane(L, torch, dev, h, mode, B[i * KB:(i + 1) * KB], X0[i * KB:(i + 1) * KB]) for i in range(NL)]
+    single = Lane(L, torch, dev, h, mode, b[None], x0[None])
     stream0 = lanes[0].stream
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=f"cuda:{dev}")
     torch.cuda.synchronize()
 
-    # single-RHS latency (solve time to 1e-10) on lane 0, with CUDA events
-    # around every finest-level launch for the kernel roofline
-    lanes[0].solve_dev()
+    # single-RHS latency (solve time to 1e-10) with CUDA events
+    single.solve_dev()
     torch.cuda.synchronize()
-    lib.lamg_ctx_profile(lanes[0].ctx.p, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream0)
-    lanes[0].solve_dev()
-    e1.record(stream0)
+    e0.record(single.stream)
+    single.solve_dev()
+    e1.record(single.stream)
     torch.cuda.synchronize()
-    single_ms, single_cycles = e0.elapsed_time(e1), lanes[0].cycles
+    if single.err:
+        raise single.err
+    single_ms, single_cycles = e0.elapsed_time(e1), single.cycles[0]
     hbm, hbm_src = peaks()
+    # finest-level kernel times (CUDA events around every finest launch) of a
+    # single-RHS solve and of one block solve
     kern = {}
-    for k, name in ((0, "gs_finest"), (1, "residual_finest")):
-        nl, tm, by = C.c_int64(), C.c_double(), C.c_double()
-        lib.lamg_ctx_profile_read(lanes[0].ctx.p, C.c_int(k), C.byref(nl), C.byref(tm), C.byref(by))
-        if nl.value:
-            avg = tm.value / nl.value
-            kern[name] = {"launches": nl.value, "avg_ms": avg, "bytes": by.value,
-                          "gbs": by.value / (avg / 1e3) / 1e9, "share": tm.value / single_ms}
-    lib.lamg_ctx_profile(lanes[0].ctx.p, 0)
+    for tag, ln in (("", single), ("_block", lanes[0])):
+        tb = time.time()
+        kp = kernel_profile(lib, ln, Lane.solve_dev, 0.0)
+        torch.cuda.synchronize()
+        if ln.err:
+            raise ln.err
+        for k, v in kp.items():
+            kern[k + tag] = v
+        log(f"[rank {dist.rank}] profiled {'block' if tag else 'single'} solve in {time.time() - tb:.1f}s")
 
     for _ in range(args.warmup):
         run_lanes(lanes, Lane.solve_dev, torch, stream0)
@@ -258,7 +310,7 @@ def run_lamg(args, dist: Dist):
     tot_units = dist.allreduce(units, "SUM")
     value = tot_units / (max_ms / 1e3)
 
-    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    dom = "gs_finest_block" if "gs_finest_block" in kern else ("gs_finest" if "gs_finest" in kern else None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and os.path.exists(tp):
@@ -268,11 +320,12 @@ def run_lamg(args, dist: Dist):
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(kern[dom]["gbs"], 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(kern[dom]["gbs"] / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
                 "algorithmic_bytes_per_launch": kern[dom]["bytes"], "avg_launch_ms": round(kern[dom]["avg_ms"], 5),
-                "share_of_single_rhs_solve": round(kern[dom]["share"], 3),
-                "measured": "CUDA events on the context stream around every finest-level launch of the "
-                            "single-RHS solve (lane 0 alone, inside bench.py)",
-                "dominant_by_time": "tail_kernel: the on-device coarse-level sub-cycle, latency-bound "
-                                    "(grid/CTA barriers per colour phase), not HBM-bound",
+                "algorithmic_bytes": "per finest Gauss-Seidel sweep: operator once (8(n+1) + 24m + 8n) plus "
+                                     "24n per right-hand side (x read, b read, x write); k=1 gives 24m + 40n + 8",
+                "measured": "CUDA events on the context stream around every finest-level launch of one profiled "
+                            "solve inside bench.py (block: one lane's 32-column solve; single: one 1-column solve)",
+                "dominant_by_time": "subtree_kernel (the per-column coarse sub-cycle below 4096 rows) and the "
+                                    "coloured sweeps of levels 1-13: latency-bound colour phases, not HBM-bound",
                 "kernels": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                             for k, v in kern.items()}}
 
@@ -291,6 +344,9 @@ def run_lamg(args, dist: Dist):
 
     extra = {}
     if dist.rank == 0 and not args.skip_validate:
+        single.solve_host()
+        xt, ct = single.x.copy(), single.cycles[0]
+        xb = lanes[0].x.copy()  # column 0 of the block (same b and x0)
         ctx0.set_mode(L.MODE_VALIDATE)
         tv = time.time()
         xv, sv = L.solve(h, b, x0, L.CycleConfig(), ctx=ctx0)
@@ -302,14 +358,16 @@ def run_lamg(args, dist: Dist):
             if g["b_sha"] == sha(b) and g["x0_sha"] == sha(x0):
                 extra["validate_mode"]["reference_cycles"] = g["cycles"]
                 extra["validate_mode"]["x_bit_identical_to_reference"] = g["x_sha"] == sha(xv)
-        xt = lanes[0].x
-        extra["throughput_mode"] = {"cycles": lanes[0].cycles,
-                                    "rel_x_diff_vs_validate": float(np.linalg.norm(xt - xv) / np.linalg.norm(xv))}
+        nv = float(np.linalg.norm(xv))
+        extra["throughput_mode"] = {"single_cycles": ct, "block_cycles": lanes[0].cycles[0],
+                                    "single_rel_x_diff_vs_validate": float(np.linalg.norm(xt - xv) / nv),
+                                    "block_rel_x_diff_vs_validate": float(np.linalg.norm(xb - xv) / nv)}
         ctx0.set_mode(mode)
 
     out = None
     if dist.rank == 0:
         cpu = None if args.no_cpu_baseline or dist.world > 1 else cpu_baseline(a, b, x0, args)
+        cyc0 = all_cycles[0]
         out = {
             "metric": "fine-level edges*cycles/s (solve to relative residual 1e-10)",
             "value": value, "unit": "edges*cycles/s", "n_gpus": dist.world, "steps": args.steps,
@@ -317,23 +375,27 @@ def run_lamg(args, dist: Dist):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded generator for BASELINE.json config %d (no dataset involved)" % args.config,
             "config": {"workload": WORKLOADS[args.config], "n": a.n, "m": a.m, "mode": args.mode,
-                       "rhs_per_step_per_gpu": S,
-                       "batching": f"{S} right-hand sides solved concurrently per GPU (one CUDA stream each) "
-                                   "over one device hierarchy; the reference arm runs one solve per host thread",
-                       "levels": h.nlevels, "cycles_per_solve": all_cycles[0], "setup_s": round(setup_s, 3),
+                       "rhs_per_step_per_gpu": nrhs,
+                       "batching": f"{NL} concurrent lanes (one context/stream each) x a block of {KB} right-hand "
+                                   "sides per lane through lamg_solve_batch_dev (node-major n x K vectors, one "
+                                   "kernel schedule per block, each column returned at its own convergence); "
+                                   "the reference arm runs one solve per host thread",
+                       "levels": h.nlevels, "cycles_per_solve": {"min": min(cyc0), "max": max(cyc0),
+                                                                 "mean": round(float(np.mean(cyc0)), 2)},
+                       "setup_s": round(setup_s, 3),
                        "single_rhs_solve_ms": round(single_ms, 2), "single_rhs_cycles": single_cycles,
                        "single_rhs_value": a.m * single_cycles / (single_ms / 1e3),
                        "l2": "L2 flushed (256 MB write) between timed steps; finest operator 183 MB > 126 MB L2",
                        "parallelism": f"replicas x{dist.world} (each GPU its own right-hand sides, no collective)"},
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "edges*cycles/s", "h2d_bytes_per_step": 16 * a.n * S,
-                    "d2h_bytes_per_step": S * (8 * a.n + 8 * (max(all_cycles[0]) + 1))},
+            "e2e": {"value": e2e_value, "unit": "edges*cycles/s", "h2d_bytes_per_step": 16 * a.n * nrhs,
+                    "d2h_bytes_per_step": nrhs * (8 * a.n + 8 * (max(cyc0) + 1))},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
         out.update(extra)
-    for ln in lanes:
+    for ln in lanes + [single]:
         ln.ctx.close()
     ctx0.close()
     return out
@@ -406,7 +468,8 @@ def main():
     ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-cycles", type=int, default=3)
-    ap.add_argument("--streams", type=int, default=32, help="concurrent right-hand sides per GPU")
+    ap.add_argument("--lanes", type=int, default=4, help="concurrent solve lanes (contexts/streams) per GPU")
+    ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..32; 1 = single solves)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")
     args = ap.parse_args()

@@ -16,22 +16,78 @@ constexpr int kBT = 256;  // threads per block of the batched kernels
 
 inline int bblocks(int64_t threads) { return (int)std::max<int64_t>(1, (threads + kBT - 1) / kBT); }
 
+// V = 4 columns per thread (two 16-byte loads per gather), K/V threads per
+// row: the row's entries are loaded once per K/V threads instead of once per
+// lane, so the instruction count per row drops ~V-fold; each column is still
+// folded in entry order (same arithmetic as one thread per column).
+constexpr int kV = 4;
+template <int K, bool SUB>
+__device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict__ col,
+                                      const double* __restrict__ val, const double* X, int64_t b, int64_t e, int k0) {
+  constexpr int U = 8;  // a 7-point row in one round: every gather in flight together
+  for (int64_t e0 = b; e0 < e; e0 += U) {
+    int32_t c[U];
+    double v[U];
+    double2 x01[U], x23[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const bool ok = e0 + j < e;
+      c[j] = ok ? __ldg(col + e0 + j) : 0;
+      v[j] = ok ? __ldg(val + e0 + j) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const double2* px = reinterpret_cast<const double2*>(X + (int64_t)c[j] * K + k0);
+      const bool ok = e0 + j < e;
+      x01[j] = ok ? px[0] : make_double2(0.0, 0.0);
+      x23[j] = ok ? px[1] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (e0 + j < e) {
+        if (SUB) {
+          s[0] = s[0] - v[j] * x01[j].x;
+          s[1] = s[1] - v[j] * x01[j].y;
+          s[2] = s[2] - v[j] * x23[j].x;
+          s[3] = s[3] - v[j] * x23[j].y;
+        } else {
+          s[0] = s[0] + v[j] * x01[j].x;
+          s[1] = s[1] + v[j] * x01[j].y;
+          s[2] = s[2] + v[j] * x23[j].x;
+          s[3] = s[3] + v[j] * x23[j].y;
+        }
+      }
+  }
+}
+
 // one colour of the permuted operator; heavy rows go to bgs_heavy_kernel
 template <int K>
 __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                   const double* __restrict__ val, const double* __restrict__ diag,
                                                   const int32_t* __restrict__ row_ids, int32_t i0, int32_t i1,
                                                   const double* __restrict__ B, double* X, const int32_t* done) {
+  constexpr int T = K / kV;  // threads per row
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t i = i0 + t / K;
-  const int k = (int)(t % K);
+  const int64_t i = i0 + t / T;
+  const int k0 = (int)(t % T) * kV;
   if (i >= i1) return;
   const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
   if (e - b > kHeavyRow) return;
-  if (done && done[k]) return;
   const int32_t u = __ldg(row_ids + i);
-  const double s = col_fold<K, true>(B[(int64_t)u * K + k], col, val, X, b, e, k);
-  X[(int64_t)u * K + k] = s / __ldg(diag + i);
+  const double2* pb = reinterpret_cast<const double2*>(B + (int64_t)u * K + k0);
+  const double2 b01 = pb[0], b23 = pb[1];
+  double s[kV] = {b01.x, b01.y, b23.x, b23.y};
+  fold4<K, true>(s, col, val, X, b, e, k0);
+  const double d = __ldg(diag + i);
+  double* px = X + (int64_t)u * K + k0;
+  if (done) {
+#pragma unroll
+    for (int q = 0; q < kV; ++q)
+      if (!done[k0 + q]) px[q] = s[q] / d;
+  } else {
+    reinterpret_cast<double2*>(px)[0] = make_double2(s[0] / d, s[1] / d);
+    reinterpret_cast<double2*>(px)[1] = make_double2(s[2] / d, s[3] / d);
+  }
 }
 
 // heavy (hub) row: 8 strided slices per column (independent of K, so a
@@ -72,14 +128,23 @@ __global__ void __launch_bounds__(kBT) bgs_heavy_kernel(const int64_t* __restric
 template <int K>
 __global__ void __launch_bounds__(kBT) bres_kernel(CSRv a, const double* __restrict__ B, const double* __restrict__ X,
                                                    double* __restrict__ R, bool skip_heavy) {
+  constexpr int T = K / kV;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t u = t / K;
-  const int k = (int)(t % K);
+  const int64_t u = t / T;
+  const int k0 = (int)(t % T) * kV;
   if (u >= a.n) return;
   const int64_t b = __ldg(a.rp + u), e = __ldg(a.rp + u + 1);
   if (skip_heavy && e - b > kHeavyRow) return;
-  const double s = col_fold<K, false>(__ldg(a.diag + u) * X[u * K + k], a.col, a.val, X, b, e, k);
-  R[u * K + k] = B[u * K + k] - s;
+  const double d = __ldg(a.diag + u);
+  const double2* pxu = reinterpret_cast<const double2*>(X + u * K + k0);
+  const double2 x01 = pxu[0], x23 = pxu[1];
+  double s[kV] = {d * x01.x, d * x01.y, d * x23.x, d * x23.y};
+  fold4<K, false>(s, a.col, a.val, X, b, e, k0);
+  const double2* pb = reinterpret_cast<const double2*>(B + u * K + k0);
+  const double2 b01 = pb[0], b23 = pb[1];
+  double2* pr = reinterpret_cast<double2*>(R + u * K + k0);
+  pr[0] = make_double2(b01.x - s[0], b01.y - s[1]);
+  pr[1] = make_double2(b23.x - s[2], b23.y - s[3]);
 }
 
 template <int K>
@@ -266,7 +331,7 @@ void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X
           count_launch(), bgs_heavy_kernel<KK><<<nh, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
                                                                    cl.row_ids.p, cl.heavy.p + cl.hptr_h[cc], B, X,
                                                                    done);
-        count_launch(), bgs_kernel<KK><<<bblocks((int64_t)(i1 - i0) * KK), kBT, 0, c.s>>>(
+        count_launch(), bgs_kernel<KK><<<bblocks((int64_t)(i1 - i0) * (KK / kV)), kBT, 0, c.s>>>(
             cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, i0, i1, B, X, done);
       }
   });
@@ -278,7 +343,7 @@ void bresidual(Ctx& c, const CSRv& a, const DColor* cl, const double* B, const d
   const int32_t nh = cl ? cl->nheavy_nat : 0;
   dispatch_k(K, [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
-    count_launch(), bres_kernel<KK><<<bblocks((int64_t)a.n * KK), kBT, 0, c.s>>>(a, B, X, R, nh > 0);
+    count_launch(), bres_kernel<KK><<<bblocks((int64_t)a.n * (KK / kV)), kBT, 0, c.s>>>(a, B, X, R, nh > 0);
     if (nh) count_launch(), bres_heavy_kernel<KK><<<nh, kBT, 0, c.s>>>(a, cl->heavy_nat.p, B, X, R);
   });
   CK_LAUNCH();

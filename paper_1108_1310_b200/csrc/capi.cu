@@ -495,6 +495,7 @@ int lamg_ctx_profile(lamg_ctx* ctx, int enable) {
     Ctx& c = ctx->c;
     c.prof.enabled = enable != 0;
     c.prof.used[0] = c.prof.used[1] = 0;
+    c.prof.bytes[0] = c.prof.bytes[1] = 0.0;
   });
 }
 
@@ -511,7 +512,7 @@ int lamg_ctx_profile_read(lamg_ctx* ctx, int kernel, int64_t* launches, double* 
     }
     *launches = c.prof.used[kernel];
     *total_ms = tot;
-    *bytes = c.prof.bytes[kernel];
+    *bytes = c.prof.used[kernel] ? c.prof.bytes[kernel] / (double)c.prof.used[kernel] : 0.0;  // mean per launch
   });
 }
 

@@ -39,7 +39,7 @@ static void prof_mark(Ctx& c, int cls, bool begin, double bytes = 0.0) {
   CK(cudaEventRecord(ev[idx], c.s));
   if (!begin) {
     ++c.prof.used[cls];
-    c.prof.bytes[cls] = bytes;
+    c.prof.bytes[cls] += bytes;  // total over the profiled launches
   }
 }
 

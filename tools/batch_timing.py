@@ -17,6 +17,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
 nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 max_cycles = int(sys.argv[4]) if len(sys.argv) > 4 else 300
+lanes = int(os.environ.get("LANES", "1"))
 a = G.grid3d_7pt(int(cfg[1:])) if cfg.startswith("g") else G.make_config(int(cfg))
 B = np.stack([G.gaussian_rhs(a.n, 1000 + j) for j in range(nrhs)])
 X0 = np.stack([G.default_x0(a.n, seed=1 + j) for j in range(nrhs)])
@@ -25,6 +26,25 @@ t = time.time()
 h = L.setup(a, ctx=ctx)
 print(f"setup {time.time() - t:.2f}s levels {h.nlevels} n {a.n} m {a.m}", flush=True)
 import torch  # noqa: E402
+
+if lanes > 1:  # concurrent blocks, one context (stream + workspace) per lane
+    import threading
+    ctxs = [L.Context(0, L.MODE_THROUGHPUT) for _ in range(lanes)]
+    out = [None] * lanes
+
+    def go(i):
+        out[i] = L.solve_batch(h, B, X0, L.CycleConfig(max_cycles=max_cycles), ctx=ctxs[i])
+
+    for r in range(reps):
+        t = time.time()
+        ths = [threading.Thread(target=go, args=(i,)) for i in range(lanes)]
+        [th.start() for th in ths]
+        [th.join() for th in ths]
+        dt = time.time() - t
+        cyc = sum(s.cycles for o in out for s in o[1])
+        print(f"lanes {lanes} rep {r}: {lanes * nrhs} rhs in {dt * 1e3:.1f} ms; edges*cycles/s {a.m * cyc / dt:.3e}",
+              flush=True)
+    sys.exit(0)
 
 for r in range(reps):
     last = r == reps - 1
