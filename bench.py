@@ -314,7 +314,11 @@ def run_lamg(args, dist: Dist):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"{args.mode}:{dom}")
+        t = json.load(open(tp)).get(f"{args.mode}:{dom}")
+        if isinstance(t, dict):  # per sweep -> per profiled launch (one gs call = nu sweeps)
+            kk = t["k"]
+            alg_sweep = 24.0 * a.m + 16.0 * a.n + 8.0 + 24.0 * a.n * kk
+            traffic = round(t["dram_bytes_per_sweep"] * kern[dom]["bytes"] / alg_sweep)
     roof = None
     if dom:
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(kern[dom]["gbs"], 1), "peak": hbm, "unit": "GB/s",
@@ -468,7 +472,7 @@ def main():
     ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-cycles", type=int, default=3)
-    ap.add_argument("--lanes", type=int, default=4, help="concurrent solve lanes (contexts/streams) per GPU")
+    ap.add_argument("--lanes", type=int, default=6, help="concurrent solve lanes (contexts/streams) per GPU")
     ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..32; 1 = single solves)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")

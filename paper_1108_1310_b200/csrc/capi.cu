@@ -482,10 +482,7 @@ int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {
   return guarded([&] {
     if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
     set_device(ctx->c);
-    if (!h->h->throughput_ready) {
-      prepare_throughput(ctx->c, *h->h);
-      h->h->throughput_ready = true;
-    }
+    h->h->ensure_throughput([&] { prepare_throughput(ctx->c, *h->h); });
   });
 }
 

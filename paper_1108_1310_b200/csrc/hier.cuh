@@ -1,7 +1,9 @@
 // hier.cuh -- device-resident hierarchy (lamg::Hierarchy, hierarchy.hpp:24-50).
 #pragma once
 
+#include <atomic>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -103,7 +105,17 @@ struct DHier {
   int device = 0;
   cudaStream_t owner_stream = nullptr;
   // throughput mode (colour-permuted copies), built on demand
-  bool throughput_ready = false;
+  std::atomic<bool> throughput_ready{false};
+  std::mutex prep_mu;  // concurrent solves on one hierarchy (one context each) build it once
+  // builds the throughput-mode data once, whichever context gets here first
+  template <class F>
+  void ensure_throughput(F&& build) {
+    if (throughput_ready.load(std::memory_order_acquire)) return;
+    std::lock_guard<std::mutex> g(prep_mu);
+    if (throughput_ready.load(std::memory_order_relaxed)) return;
+    build();
+    throughput_ready.store(true, std::memory_order_release);
+  }
   uint64_t uid = next_uid();  // workspaces key on this, not on the address
   static uint64_t next_uid() {
     static std::atomic<uint64_t> c{1};

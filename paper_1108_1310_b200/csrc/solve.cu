@@ -439,10 +439,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   if (std::fabs(b_sum) > 1e-10 * b_inf)
     throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
 
-  if (!exact && !h.throughput_ready) {
-    prepare_throughput(c, const_cast<DHier&>(h));
-    const_cast<DHier&>(h).throughput_ready = true;
-  }
+  if (!exact) const_cast<DHier&>(h).ensure_throughput([&] { prepare_throughput(c, const_cast<DHier&>(h)); });
   if (!c.ws) c.ws = new Workspace();
   Workspace& ws = *c.ws;
   ws.ensure(c, h);
@@ -570,10 +567,7 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
   const int64_t n = L0.op.n;
   const int K = batch_width_for(nrhs);
   res.assign(nrhs, SolveResult{});
-  if (!h.throughput_ready) {
-    prepare_throughput(c, const_cast<DHier&>(h));
-    const_cast<DHier&>(h).throughput_ready = true;
-  }
+  const_cast<DHier&>(h).ensure_throughput([&] { prepare_throughput(c, const_cast<DHier&>(h)); });
   if (!c.bws) c.bws = new Workspace();
   Workspace& ws = *c.bws;
   ws.ensure(c, h, K);
