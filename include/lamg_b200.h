@@ -59,6 +59,7 @@ enum {
 
 typedef struct lamg_ctx lamg_ctx;
 typedef struct lamg_hier lamg_hier;
+typedef struct lamg_graph lamg_graph; /* a device-resident CSR Laplacian (graph ingest) */
 
 typedef struct {
   int32_t n;
@@ -173,6 +174,21 @@ int lamg_solve_batch(lamg_ctx *ctx, const lamg_hier *h, int32_t nrhs, const doub
 int lamg_solve_batch_dev(lamg_ctx *ctx, const lamg_hier *h, int32_t nrhs, const double *d_b,
                          const double *d_x0, const lamg_cycle_cfg *cfg, double *d_x,
                          lamg_solve_stats *stats, double *residuals, int32_t residuals_cap);
+/* ---- graph ingest on the device -----------------
+ * R-MAT of BASELINE.json config 5: 2^scale nodes,
+ * edge_factor*2^scale samples, quadrant per bit by draw t*S+i of the
+ * counter-form lamg::Rng(seed) (rng.hpp:10-41) against a, a+b, a+b+c;
+ * self-loops dropped, duplicates summed into integer weights; keep_lcc keeps
+ * the largest component in ascending node order (components.cpp:35-56).
+ * lamg_graph_lcc does the component step alone for any CSR Laplacian.
+ * lamg_graph_csr gives device pointers for lamg_setup(..., on_device=1, ...). */
+int lamg_gen_rmat(lamg_ctx *ctx, int32_t scale, int32_t edge_factor, double a, double b, double c,
+                  uint64_t seed, int32_t keep_lcc, lamg_graph **out);
+int lamg_graph_lcc(lamg_ctx *ctx, const lamg_csr *a, int on_device, lamg_graph **out);
+int lamg_graph_csr(const lamg_graph *g, lamg_csr *out_device_view);
+int lamg_graph_download(const lamg_graph *g, int64_t *row_ptr, int32_t *col, double *val, double *diag);
+void lamg_graph_destroy(lamg_graph *g);
+
 /* builds (once) the throughput-mode colour-permuted copies of the hierarchy */
 int lamg_hier_prepare_throughput(lamg_ctx *ctx, lamg_hier *h);
 

@@ -64,6 +64,7 @@ def lib():
         L.lamg_rng_derive.argtypes = [C.c_uint64, C.c_uint64]
         L.lamg_ctx_destroy.restype = None
         L.lamg_hier_destroy.restype = None
+        L.lamg_graph_destroy.restype = None
         _lib = L
     return _lib
 

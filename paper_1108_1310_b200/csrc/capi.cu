@@ -223,6 +223,16 @@ int solve_batch_common(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const do
 
 }  // namespace
 
+namespace lamgb {
+void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc, uint64_t seed, bool lcc, DCSR& out);
+bool largest_component_dev(Ctx& c, const CSRv& a, DCSR& out);
+}  // namespace lamgb
+
+struct lamg_graph {
+  int device = 0;
+  DCSR a;
+};
+
 extern "C" {
 
 const char* lamg_last_error(void) { return g_err.c_str(); }
@@ -476,6 +486,84 @@ int lamg_solve_batch_dev(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const 
                          const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
                          int32_t cap) {
   return solve_batch_common(ctx, h, nrhs, b, x0, true, cfg, x, stats, residuals, cap);
+}
+
+// ------------------------------------------------------ graph ingest (gen.cu)
+int lamg_gen_rmat(lamg_ctx* ctx, int32_t scale, int32_t edge_factor, double a, double b, double c_, uint64_t seed,
+                  int32_t keep_lcc, lamg_graph** out) {
+  *out = nullptr;
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    auto* g = new lamg_graph();
+    g->device = c.device;
+    try {
+      gen_rmat(c, scale, edge_factor, a, b, c_, seed, keep_lcc != 0, g->a);
+      c.sync();
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int lamg_graph_lcc(lamg_ctx* ctx, const lamg_csr* a, int on_device, lamg_graph** out) {
+  *out = nullptr;
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    auto* g = new lamg_graph();
+    g->device = c.device;
+    try {
+      DCSR up;
+      CSRv v{a->n, a->m, a->row_ptr, a->col, a->val, a->diag};
+      if (!on_device) {
+        upload_csr(c, a, up);
+        v = up.view();
+      }
+      if (!largest_component_dev(c, v, g->a)) {  // already connected: a copy
+        g->a.alloc(v.n, v.m, c.s);
+        CK(cudaMemcpyAsync(g->a.rp.p, v.rp, sizeof(int64_t) * (v.n + 1), cudaMemcpyDefault, c.s));
+        CK(cudaMemcpyAsync(g->a.col.p, v.col, sizeof(int32_t) * 2 * v.m, cudaMemcpyDefault, c.s));
+        CK(cudaMemcpyAsync(g->a.val.p, v.val, sizeof(double) * 2 * v.m, cudaMemcpyDefault, c.s));
+        CK(cudaMemcpyAsync(g->a.diag.p, v.diag, sizeof(double) * v.n, cudaMemcpyDefault, c.s));
+      }
+      c.sync();
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int lamg_graph_csr(const lamg_graph* g, lamg_csr* out) {
+  return guarded([&] {
+    if (!g) throw LamgError(LAMG_E_ARGUMENT, "null graph");
+    *out = lamg_csr{g->a.n, g->a.m, g->a.rp.p, g->a.col.p, g->a.val.p, g->a.diag.p};
+  });
+}
+
+int lamg_graph_download(const lamg_graph* g, int64_t* row_ptr, int32_t* col, double* val, double* diag) {
+  return guarded([&] {
+    if (!g) throw LamgError(LAMG_E_ARGUMENT, "null graph");
+    CK(cudaSetDevice(g->device));
+    CK(cudaDeviceSynchronize());
+    if (row_ptr) CK(cudaMemcpy(row_ptr, g->a.rp.p, sizeof(int64_t) * (g->a.n + 1), cudaMemcpyDeviceToHost));
+    if (col) CK(cudaMemcpy(col, g->a.col.p, sizeof(int32_t) * 2 * g->a.m, cudaMemcpyDeviceToHost));
+    if (val) CK(cudaMemcpy(val, g->a.val.p, sizeof(double) * 2 * g->a.m, cudaMemcpyDeviceToHost));
+    if (diag) CK(cudaMemcpy(diag, g->a.diag.p, sizeof(double) * g->a.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+void lamg_graph_destroy(lamg_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  cudaDeviceSynchronize();
+  g_free_sync = true;
+  delete g;
+  g_free_sync = false;
 }
 
 int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {

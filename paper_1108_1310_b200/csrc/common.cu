@@ -137,6 +137,10 @@ void sort_pairs_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, const int64_t* 
   if (n <= 0) return;
   CUB_TWICE(cub::DeviceRadixSort::SortPairs(tmp_, bytes_, kin, kout, vin, vout, (size_t)n, 0, bits, c.s));
 }
+void sort_keys_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, int64_t n, int bits) {
+  if (n <= 0) return;
+  CUB_TWICE(cub::DeviceRadixSort::SortKeys(tmp_, bytes_, kin, kout, (size_t)n, 0, bits, c.s));
+}
 void sort_pairs_u64_d(Ctx& c, const uint64_t* kin, uint64_t* kout, const double* vin, double* vout,
                       int64_t n, int bits) {
   if (n <= 0) return;

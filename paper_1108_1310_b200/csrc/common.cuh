@@ -369,6 +369,7 @@ void coop_launch(Ctx& c, const void* kernel, int blocks, int threads, void** arg
 // stable LSD radix sort of (key, value) pairs on the low `bits` key bits
 void sort_pairs_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, const int64_t* vin,
                     int64_t* vout, int64_t n, int bits);
+void sort_keys_u64(Ctx& c, const uint64_t* kin, uint64_t* kout, int64_t n, int bits);
 void sort_pairs_u64_d(Ctx& c, const uint64_t* kin, uint64_t* kout, const double* vin,
                       double* vout, int64_t n, int bits);
 void sort_pairs_u32_i32(Ctx& c, const uint32_t* kin, uint32_t* kout, const int32_t* vin,

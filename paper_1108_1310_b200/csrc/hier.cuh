@@ -123,6 +123,11 @@ struct DHier {
   }
 };
 
+// assemble_canonical (sparse_laplacian.cpp:60-104) of a sorted, merged u<v
+// edge list on the device (setup.cu)
+void assemble_canonical_dev(Ctx& c, int32_t n, int64_t E, const int32_t* eu, const int32_t* ev, const double* ew,
+                            DCSR& out);
+
 struct SetupOpts {
   double gamma = 1.5;
   uint64_t seed = 1;

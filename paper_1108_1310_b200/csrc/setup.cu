@@ -96,7 +96,7 @@ __global__ void narrow_kernel(const uint64_t* in, int64_t n, int32_t* out) {
   if (i < n) out[i] = (int32_t)in[i];
 }
 
-static void assemble_canonical_dev(Ctx& c, int32_t n, int64_t E, const int32_t* eu,
+void assemble_canonical_dev(Ctx& c, int32_t n, int64_t E, const int32_t* eu,
                                    const int32_t* ev, const double* ew, DCSR& out) {
   if (n <= 0) throw LamgError(LAMG_E_EMPTY_GRAPH, "cannot assemble a Laplacian with n = 0");
   out.alloc(n, E, c.s);

@@ -324,16 +324,72 @@ class Hierarchy:
 # ---------------------------------------------------------------- drivers
 def setup(a, opts: SetupOptions | None = None, ctx: Context | None = None, seed: int | None = None,
           **kw) -> Hierarchy:
-    """lamg::setup (hierarchy.hpp:65) on the GPU."""
+    """lamg::setup (hierarchy.hpp:65) on the GPU. `a` is a host CSR or a
+    DeviceGraph (already in HBM)."""
     ctx = ctx or default_context()
     opts = opts or SetupOptions(**kw)
     if seed is not None:
         opts.rng_seed = seed
-    arg = _CSRArg(a)
     h = C.c_void_p()
     o = opts.c()
-    _check(ctx.lib.lamg_setup(ctx.p, arg.ref(), C.c_int(0), C.byref(o), C.byref(h)))
+    if isinstance(a, DeviceGraph):
+        _check(ctx.lib.lamg_setup(ctx.p, C.byref(a.csr), C.c_int(1), C.byref(o), C.byref(h)))
+    else:
+        arg = _CSRArg(a)
+        _check(ctx.lib.lamg_setup(ctx.p, arg.ref(), C.c_int(0), C.byref(o), C.byref(h)))
     return Hierarchy(ctx, h, int(a.n))
+
+
+class DeviceGraph:
+    """A CSR Laplacian resident in HBM (lamg_graph): the output of the device
+    generators / component extraction (gen.cu)."""
+
+    def __init__(self, ctx: Context, g):
+        self.ctx, self.g = ctx, g
+        self.csr = _lib.lamg_csr()
+        _check(ctx.lib.lamg_graph_csr(g, C.byref(self.csr)))
+        self.n, self.m = int(self.csr.n), int(self.csr.m)
+
+    def download(self):
+        """Host copy with the SparseLaplacian field names."""
+        from .graphs import SparseLaplacian
+        rp = np.empty(self.n + 1, dtype=np.int64)
+        col = np.empty(2 * self.m, dtype=np.int32)
+        val = np.empty(2 * self.m)
+        diag = np.empty(self.n)
+        _check(self.ctx.lib.lamg_graph_download(self.g, _p(rp), _p(col), _p(val), _p(diag)))
+        return SparseLaplacian(self.n, self.m, rp, col, val, diag)
+
+    def close(self):
+        if self.g:
+            self.ctx.lib.lamg_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
+def gen_rmat(scale: int, seed: int = 5, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0.05), lcc: bool = True,
+             ctx: Context | None = None) -> DeviceGraph:
+    """BASELINE config 5 generator on the device; bit-identical to graphs.rmat."""
+    ctx = ctx or default_context()
+    a, b, c, _ = abcd
+    g = C.c_void_p()
+    _check(ctx.lib.lamg_gen_rmat(ctx.p, C.c_int32(scale), C.c_int32(edge_factor), C.c_double(a), C.c_double(b),
+                                 C.c_double(c), C.c_uint64(seed), C.c_int32(int(lcc)), C.byref(g)))
+    return DeviceGraph(ctx, g)
+
+
+def largest_component(a, ctx: Context | None = None) -> DeviceGraph:
+    """graphs.largest_component on the device (union-find, ascending order)."""
+    ctx = ctx or default_context()
+    arg = _CSRArg(a)
+    g = C.c_void_p()
+    _check(ctx.lib.lamg_graph_lcc(ctx.p, arg.ref(), C.c_int(0), C.byref(g)))
+    return DeviceGraph(ctx, g)
 
 
 def solve(h: Hierarchy, b, x0, cfg: CycleConfig | None = None, ctx: Context | None = None):
