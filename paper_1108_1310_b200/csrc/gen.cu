@@ -68,7 +68,10 @@ __global__ void iota_i32_kernel(int32_t* p, int32_t n) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = i;
 }
-__device__ inline int32_t find_root(int32_t* parent, int32_t x) {
+// parent links only ever point to smaller ids; reads bypass L1 (another SM
+// may have linked a root since this SM cached the line)
+__device__ inline int32_t find_root(int32_t* parent_, int32_t x) {
+  volatile int32_t* parent = parent_;
   int32_t p = parent[x];
   while (p != x) {  // path halving; racing writes only shorten paths
     const int32_t g = parent[p];
@@ -92,6 +95,11 @@ __global__ void hook_kernel(const int32_t* eu, const int32_t* ev, int64_t E, int
     a = lo;
     b = hi;
   }
+}
+// edges whose endpoints still have different roots (union retry guard)
+__global__ void unjoined_kernel(const int32_t* eu, const int32_t* ev, int64_t E, int32_t* parent, int32_t* flag) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < E && find_root(parent, eu[e]) != find_root(parent, ev[e])) *flag = 1;
 }
 __global__ void compress_kernel(int32_t* parent, int32_t n, int32_t* size) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -163,7 +171,17 @@ bool largest_component_dev(Ctx& c, const CSRv& a, DCSR& out) {
   DVec<int32_t> parent(n, c.s), size(n, c.s);
   count_launch(), iota_i32_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(parent.p, n);
   size.zero();
-  if (E) count_launch(), hook_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(eu.p, ev.p, E, parent.p);
+  // hook until every edge joins one tree (one pass in practice; the check
+  // makes the result independent of any interleaving)
+  int32_t* unjoined = c.dflag + 40;
+  for (int pass = 0; E && pass < 64; ++pass) {
+    count_launch(), hook_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(eu.p, ev.p, E, parent.p);
+    CK(cudaMemsetAsync(unjoined, 0, sizeof(int32_t), c.s));
+    count_launch(), unjoined_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(eu.p, ev.p, E, parent.p, unjoined);
+    CK_LAUNCH();
+    if (read_i32(c, unjoined) == 0) break;
+    if (pass == 63) throw LamgError(LAMG_E_ERROR, "largest component: union-find did not converge");
+  }
   count_launch(), compress_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(parent.p, n, size.p);
   unsigned long long* best = (unsigned long long*)(c.dscal + 96);
   CK(cudaMemsetAsync(best, 0, sizeof(unsigned long long), c.s));
