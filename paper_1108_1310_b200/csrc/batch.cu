@@ -60,7 +60,7 @@ __device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict
   }
 }
 
-// one colour of the permuted operator; heavy rows go to bgs_heavy_kernel
+// one colour of the permuted operator; rows longer than kLongRow go to the long-row kernels
 template <int K>
 __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                   const double* __restrict__ val, const double* __restrict__ diag,
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp
   const int k0 = (int)(t % T) * kV;
   if (i >= i1) return;
   const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
-  if (e - b > kHeavyRow) return;
+  if (e - b > kLongRow) return;  // bgs_long_kernel / blong_*_kernel
   const int32_t u = __ldg(row_ids + i);
   const double2* pb = reinterpret_cast<const double2*>(B + (int64_t)u * K + k0);
   const double2 b01 = pb[0], b23 = pb[1];
@@ -90,51 +90,125 @@ __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp
   }
 }
 
-// heavy (hub) row: 8 strided slices per column (independent of K, so a
-// column's sum is the same in every batch), slice partials folded in order
-constexpr int kHS = 8;
+// Long rows (more than kLongRow entries): one CTA per row -- or per chunk of
+// kChunk entries for the longest -- folds 32 strided slices of the entries
+// for all K columns; slice partials combine in slice order, chunk sums in
+// chunk order. The order depends on the row only, never on K.
+constexpr int kSL = 32;
 template <int K>
-__device__ __forceinline__ double heavy_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
-                                            const double* X, int64_t b, int64_t e) {
-  __shared__ double sh[kHS * 32];
-  for (int pr = threadIdx.x; pr < kHS * K; pr += blockDim.x) {
-    const int sl = pr / K, k = pr % K;
-    double p = 0.0;
-    for (int64_t j = b + sl; j < e; j += kHS) p += __ldg(val + j) * X[(int64_t)__ldg(col + j) * K + k];
-    sh[sl * K + k] = p;
+__device__ __forceinline__ void fold4_strided(double (&s)[kV], const int32_t* __restrict__ col,
+                                              const double* __restrict__ val, const double* X, int64_t j0,
+                                              int64_t e, int k0) {
+  constexpr int U = 8;
+  for (int64_t base = j0; base < e; base += (int64_t)U * kSL) {
+    int32_t c[U];
+    double v[U];
+    double2 x01[U], x23[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t j = base + (int64_t)q * kSL;
+      const bool ok = j < e;
+      c[q] = ok ? __ldg(col + j) : 0;
+      v[q] = ok ? __ldg(val + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const double2* px = reinterpret_cast<const double2*>(X + (int64_t)c[q] * K + k0);
+      const bool ok = base + (int64_t)q * kSL < e;
+      x01[q] = ok ? px[0] : make_double2(0.0, 0.0);
+      x23[q] = ok ? px[1] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (base + (int64_t)q * kSL < e) {
+        s[0] = s[0] + v[q] * x01[q].x;
+        s[1] = s[1] + v[q] * x01[q].y;
+        s[2] = s[2] + v[q] * x23[q].x;
+        s[3] = s[3] + v[q] * x23[q].y;
+      }
+  }
+}
+// sum over entries [cb, ce) for this CTA's K columns; valid in threads [0, K)
+template <int K>
+__device__ __forceinline__ double long_chunk_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                 const double* X, int64_t cb, int64_t ce) {
+  __shared__ double sh[kSL * 32];
+  constexpr int Q = K / kV;
+  for (int pr = threadIdx.x; pr < kSL * Q; pr += blockDim.x) {
+    const int sl = pr / Q, k0 = (pr % Q) * kV;
+    double s[kV] = {0.0, 0.0, 0.0, 0.0};
+    fold4_strided<K>(s, col, val, X, cb + sl, ce, k0);
+#pragma unroll
+    for (int q = 0; q < kV; ++q) sh[sl * K + k0 + q] = s[q];
   }
   __syncthreads();
   double t = 0.0;
   if ((int)threadIdx.x < K)
-    for (int q = 0; q < kHS; ++q) t += sh[q * K + threadIdx.x];
-  return t;  // valid in threads [0, K)
+    for (int sl = 0; sl < kSL; ++sl) t += sh[sl * K + threadIdx.x];
+  return t;
 }
 
 template <int K>
-__global__ void __launch_bounds__(kBT) bgs_heavy_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                                        const double* __restrict__ val, const double* __restrict__ diag,
-                                                        const int32_t* __restrict__ row_ids,
-                                                        const int32_t* __restrict__ heavy, const double* __restrict__ B,
-                                                        double* X, const int32_t* done) {
-  const int32_t i = heavy[blockIdx.x];
-  const double dot = heavy_dot<K>(col, val, X, rp[i], rp[i + 1]);
+__global__ void __launch_bounds__(kBT) bgs_long_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val, const double* __restrict__ diag,
+                                                       const int32_t* __restrict__ row_ids,
+                                                       const int32_t* __restrict__ rows, const double* __restrict__ B,
+                                                       double* X, const int32_t* done) {
+  const int32_t i = rows[blockIdx.x];
+  const double t = long_chunk_dot<K>(col, val, X, rp[i], rp[i + 1]);
   const int k = threadIdx.x;
   if (k < K && !(done && done[k])) {
-    const int32_t u = row_ids[i];
-    X[(int64_t)u * K + k] = (B[(int64_t)u * K + k] - dot) / diag[i];
+    const int64_t u = row_ids[i];
+    X[u * K + k] = (B[u * K + k] - t) / diag[i];
+  }
+}
+// one CTA per (super-long row, chunk) work item: chunk sums to scratch
+template <int K>
+__global__ void __launch_bounds__(kBT) blong_part_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const int32_t* __restrict__ item_row,
+                                                         const int32_t* __restrict__ item_chunk, int32_t it0,
+                                                         const double* X, double* scratch) {
+  const int32_t it = it0 + blockIdx.x;
+  const int32_t i = item_row[it];
+  const int64_t cb = rp[i] + (int64_t)item_chunk[it] * kChunk;
+  const int64_t ce = cb + kChunk < rp[i + 1] ? cb + kChunk : rp[i + 1];
+  const double t = long_chunk_dot<K>(col, val, X, cb, ce);
+  if ((int)threadIdx.x < K) scratch[(int64_t)it * K + threadIdx.x] = t;
+}
+// chunk sums in chunk order -> the row's update (GS: stored rows; residual:
+// natural rows, row_ids == nullptr)
+template <int K, bool RES>
+__global__ void blong_fin_kernel(const int32_t* __restrict__ srows, const int32_t* __restrict__ sitem0, int32_t s0,
+                                 int32_t ns, const double* __restrict__ scratch, const int32_t* __restrict__ row_ids,
+                                 const double* __restrict__ diag, const double* __restrict__ B, double* X, double* R,
+                                 const int32_t* done) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ns * K) return;
+  const int32_t s = s0 + (int32_t)(t / K);
+  const int k = (int)(t % K);
+  double tot = 0.0;
+  for (int32_t it = sitem0[s]; it < sitem0[s + 1]; ++it) tot += scratch[(int64_t)it * K + k];
+  const int32_t i = srows[s];
+  if (RES) {
+    const int64_t q = (int64_t)i * K + k;
+    R[q] = B[q] - (diag[i] * X[q] + tot);
+  } else if (!(done && done[k])) {
+    const int64_t u = row_ids[i];
+    X[u * K + k] = (B[u * K + k] - tot) / diag[i];
   }
 }
 
 template <int K>
 __global__ void __launch_bounds__(kBT) bres_kernel(CSRv a, const double* __restrict__ B, const double* __restrict__ X,
-                                                   double* __restrict__ R, bool skip_heavy) {
+                                                   double* __restrict__ R) {
   constexpr int T = K / kV;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t u = t / T;
   const int k0 = (int)(t % T) * kV;
   if (u >= a.n) return;
   const int64_t b = __ldg(a.rp + u), e = __ldg(a.rp + u + 1);
-  if (skip_heavy && e - b > kHeavyRow) return;
+  if (e - b > kLongRow) return;  // bres_long_kernel / blong_*_kernel
   const double d = __ldg(a.diag + u);
   const double2* pxu = reinterpret_cast<const double2*>(X + u * K + k0);
   const double2 x01 = pxu[0], x23 = pxu[1];
@@ -148,12 +222,15 @@ __global__ void __launch_bounds__(kBT) bres_kernel(CSRv a, const double* __restr
 }
 
 template <int K>
-__global__ void __launch_bounds__(kBT) bres_heavy_kernel(CSRv a, const int32_t* __restrict__ heavy,
-                                                         const double* __restrict__ B, const double* X, double* R) {
-  const int32_t u = heavy[blockIdx.x];
-  const double dot = heavy_dot<K>(a.col, a.val, X, a.rp[u], a.rp[u + 1]);
+__global__ void __launch_bounds__(kBT) bres_long_kernel(CSRv a, const int32_t* __restrict__ rows,
+                                                        const double* __restrict__ B, const double* X, double* R) {
+  const int32_t u = rows[blockIdx.x];
+  const double t = long_chunk_dot<K>(a.col, a.val, X, a.rp[u], a.rp[u + 1]);
   const int k = threadIdx.x;
-  if (k < K) R[(int64_t)u * K + k] = B[(int64_t)u * K + k] - (a.diag[u] * X[(int64_t)u * K + k] + dot);
+  if (k < K) {
+    const int64_t q = (int64_t)u * K + k;
+    R[q] = B[q] - (a.diag[u] * X[q] + t);
+  }
 }
 
 template <int K>
@@ -317,34 +394,59 @@ void dispatch_k(int K, F&& f) {
 
 }  // namespace
 
+static double* long_scratch(Ctx& c, const LongRows& L, int K) {
+  const int64_t need = std::max<int64_t>((int64_t)L.iptr_h.back() * K, 1);
+  if (c.bscratch.n < need) c.bscratch.alloc(need, c.s);
+  return c.bscratch.p;
+}
+
 void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X, int sweeps, int K,
                  const int32_t* done) {
   if (n == 0 || sweeps <= 0) return;
+  const LongRows& L = cl.blong;
+  double* scratch = long_scratch(c, L, K);
   dispatch_k(K, [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
     for (int sw = 0; sw < sweeps; ++sw)
       for (int32_t cc = 0; cc < cl.ncolors; ++cc) {
         const int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
         if (i1 <= i0) continue;
-        const int32_t nh = cl.hptr_h.empty() ? 0 : cl.hptr_h[cc + 1] - cl.hptr_h[cc];
-        if (nh)
-          count_launch(), bgs_heavy_kernel<KK><<<nh, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
-                                                                   cl.row_ids.p, cl.heavy.p + cl.hptr_h[cc], B, X,
-                                                                   done);
         count_launch(), bgs_kernel<KK><<<bblocks((int64_t)(i1 - i0) * (KK / kV)), kBT, 0, c.s>>>(
             cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, i0, i1, B, X, done);
+        const int32_t nl = L.ptr_h[cc + 1] - L.ptr_h[cc];
+        if (nl)
+          count_launch(), bgs_long_kernel<KK><<<nl, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
+                                                                  cl.row_ids.p, L.rows.p + L.ptr_h[cc], B, X, done);
+        const int32_t ni = L.iptr_h[cc + 1] - L.iptr_h[cc];
+        if (ni) {
+          count_launch(), blong_part_kernel<KK><<<ni, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, L.item_row.p,
+                                                                    L.item_chunk.p, L.iptr_h[cc], X, scratch);
+          const int32_t ns = L.sptr_h[cc + 1] - L.sptr_h[cc];
+          count_launch(), blong_fin_kernel<KK, false><<<bblocks((int64_t)ns * KK), kBT, 0, c.s>>>(
+              L.srows.p, L.sitem0.p, L.sptr_h[cc], ns, scratch, cl.row_ids.p, cl.diag.p, B, X, nullptr, done);
+        }
       }
   });
   CK_LAUNCH();
 }
 
-void bresidual(Ctx& c, const CSRv& a, const DColor* cl, const double* B, const double* X, double* R, int K) {
+void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const double* X, double* R, int K) {
   if (a.n == 0) return;
-  const int32_t nh = cl ? cl->nheavy_nat : 0;
+  if (L.ptr_h.empty()) throw LamgError(LAMG_E_ERROR, "batched residual needs the level's throughput data");
+  double* scratch = long_scratch(c, L, K);
   dispatch_k(K, [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
-    count_launch(), bres_kernel<KK><<<bblocks((int64_t)a.n * (KK / kV)), kBT, 0, c.s>>>(a, B, X, R, nh > 0);
-    if (nh) count_launch(), bres_heavy_kernel<KK><<<nh, kBT, 0, c.s>>>(a, cl->heavy_nat.p, B, X, R);
+    count_launch(), bres_kernel<KK><<<bblocks((int64_t)a.n * (KK / kV)), kBT, 0, c.s>>>(a, B, X, R);
+    const int32_t nl = L.ptr_h[1];
+    if (nl) count_launch(), bres_long_kernel<KK><<<nl, kBT, 0, c.s>>>(a, L.rows.p, B, X, R);
+    const int32_t ni = L.iptr_h[1];
+    if (ni) {
+      count_launch(), blong_part_kernel<KK><<<ni, kBT, 0, c.s>>>(a.rp, a.col, a.val, L.item_row.p, L.item_chunk.p, 0,
+                                                                X, scratch);
+      const int32_t ns = L.sptr_h[1];
+      count_launch(), blong_fin_kernel<KK, true><<<bblocks((int64_t)ns * KK), kBT, 0, c.s>>>(
+          L.srows.p, L.sitem0.p, 0, ns, scratch, nullptr, a.diag, B, const_cast<double*>(X), R, nullptr);
+    }
   });
   CK_LAUNCH();
 }
@@ -444,15 +546,15 @@ void column_out(Ctx& c, const double* X, int64_t n, int K, int k, double* dst, c
   CK_LAUNCH();
 }
 
-void brelax(Ctx& c, const CSRv& a, const DColor& cl, const double* B, double* X, double* R, int K,
-            std::vector<int>& sweeps) {
+void brelax(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* B, double* X, double* R,
+            int K, std::vector<int>& sweeps) {
   sweeps.assign(K, 0);
   int32_t* done = c.dbdone;
   double* nrm = c.dbscal;          // [K]
   double* sums = c.dbscal + 64;    // [K]
   std::vector<double> r0(K), rn(K);
   std::vector<int32_t> hdone(K, 0);
-  bresidual(c, a, &cl, B, X, R, K);
+  bresidual(c, a, nat, B, X, R, K);
   c.work += (double)a.m;
   bcolsum(c, R, a.n, K, true, nrm);
   CK(cudaMemcpyAsync(rn.data(), nrm, K * sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -469,7 +571,7 @@ void brelax(Ctx& c, const CSRv& a, const DColor& cl, const double* B, double* X,
     c.work += (double)a.m;
     bcolsum(c, X, a.n, K, false, sums);
     bsub_mean(c, X, a.n, K, sums, done);
-    bresidual(c, a, &cl, B, X, R, K);
+    bresidual(c, a, nat, B, X, R, K);
     c.work += (double)a.m;
     bcolsum(c, R, a.n, K, true, nrm);
     CK(cudaMemcpyAsync(rn.data(), nrm, K * sizeof(double), cudaMemcpyDeviceToHost, c.s));

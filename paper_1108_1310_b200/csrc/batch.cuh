@@ -46,7 +46,7 @@ inline bool batch_width_ok(int K) { return K == 4 || K == 8 || K == 16 || K == 3
 
 void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X, int sweeps, int K,
                  const int32_t* done = nullptr);
-void bresidual(Ctx& c, const CSRv& a, const DColor* cl, const double* B, const double* X, double* R, int K);
+void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const double* X, double* R, int K);
 void brestrict(Ctx& c, int32_t coarse_n, const int64_t* mem_ptr, const int32_t* mem, const double* R, double mu,
                double* Bc, double* Xc, int K);
 void binterpolate(Ctx& c, int32_t fine_n, const int32_t* agg, const double* Xc, double* X, int K);
@@ -65,7 +65,7 @@ void column_out(Ctx& c, const double* X, int64_t n, int K, int k, double* dst, c
 inline int batch_width_for(int nrhs) { return nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : nrhs <= 16 ? 16 : 32; }
 // RelaxationSolver::solve (coarse_solver.cpp:82-93) per column; returns the
 // sweeps of every column in sweeps[K]
-void brelax(Ctx& c, const CSRv& a, const DColor& cl, const double* B, double* X, double* R, int K,
-            std::vector<int>& sweeps);
+void brelax(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* B, double* X, double* R,
+            int K, std::vector<int>& sweeps);
 
 }  // namespace lamgb

@@ -287,6 +287,7 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   c.ws = nullptr;
   delete c.bws;
   c.bws = nullptr;
+  c.bscratch.release();
   c.res_csr = DCSR();
   c.res_stage.f_diag.release();
   c.res_stage.f_ptr.release();

@@ -199,6 +199,7 @@ struct Ctx {
   double* dbpart = nullptr;     // batched reductions: per-column chunk partials (32 x kColChunks)
   double* dbscal = nullptr;     // batched scalars (256 doubles)
   int32_t* dbdone = nullptr;    // batched per-column masks (64 ints)
+  DVec<double> bscratch;        // batched long-row chunk sums (grown on demand)
   // per-kernel API results kept until taken
   DCSR res_csr;
   struct {

@@ -58,6 +58,20 @@ struct DDirect {
   DVec<int64_t> inv_off;           // [ncomp] offsets into inv
 };
 
+// blocks of K columns (batch.cu): rows longer than kLongRow are reduced by
+// a CTA in 32 strided slices; rows longer than kChunk are split into chunks
+// of kChunk entries (one CTA each) whose sums combine in chunk order
+struct LongRows {
+  DVec<int32_t> rows;                  // long rows (> kLongRow entries, <= kChunk)
+  std::vector<int32_t> ptr_h;          // per colour (stored order) or [0, count] (natural)
+  DVec<int32_t> item_row, item_chunk;  // super-long rows: (row, chunk) work items
+  std::vector<int32_t> iptr_h;
+  DVec<int32_t> srows, sitem0;         // super-long rows and their first item
+  std::vector<int32_t> sptr_h;
+};
+// lists over the row ranges `bounds` of a CSR with host row pointers rp
+void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<int32_t>& bounds, LongRows& L);
+
 // Throughput-mode smoother data: a greedy first-fit colouring in index order
 // (computed over the exact-order wavefronts, so it is the sequential greedy
 // colouring) and a copy of the operator whose rows are stored colour by
@@ -78,7 +92,10 @@ struct DColor {
   DVec<int32_t> hptr;
   DVec<int32_t> heavy_nat;      // natural rows with more than kHeavyRow entries
   int32_t nheavy_nat = 0;
+  LongRows blong;  // stored (colour) order, ranges per colour
 };
+constexpr int64_t kLongRow = 64;
+constexpr int64_t kChunk = 16384;
 
 constexpr int64_t kHeavyRow = 2048;
 
@@ -93,6 +110,7 @@ struct DLevel {
   std::unique_ptr<DDirect> direct;
   Schedule sched;          // exact-order GS wavefronts of this level's operator
   std::unique_ptr<DColor> color;  // throughput-mode coloured operator (on demand)
+  LongRows blong_nat;             // throughput mode: long rows in natural order (K-column residuals)
   UpperIndex upper;        // energy / relaxation helpers
 };
 

@@ -253,7 +253,7 @@ struct Driver {
       } else {
         if (!L.color) throw LamgError(LAMG_E_ERROR, "batched relaxation needs the coloured operator");
         std::vector<int> sw;
-        brelax(c, L.op.view(), *L.color, b, x, ws.lv[l].r.p, K, sw);
+        brelax(c, L.op.view(), *L.color, L.blong_nat, b, x, ws.lv[l].r.p, K, sw);
         relax_cols.resize(K, 0);
         for (int k = 0; k < K; ++k) relax_cols[k] += sw[k];
       }
@@ -345,7 +345,7 @@ struct Driver {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
-    if (K > 1) bresidual(c, L.op.view(), L.color.get(), b, x, r, K);
+    if (K > 1) bresidual(c, L.op.view(), L.blong_nat, b, x, r, K);
     else if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
     else residual_exact(c, L.op.view(), b, x, r, L.sched.heavy_nat.p, L.sched.nheavy_nat);
     if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K);

@@ -138,6 +138,53 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   out.heavy_nat.alloc(n, c.s);
   out.nheavy_nat = (int32_t)select_flagged_index(c, hf.p, out.heavy_nat.p, n);
   c.sync();
+  // long-row lists for the K-column kernels (batch.cu)
+  std::vector<int64_t> prp((size_t)n + 1);
+  out.rp.download(prp.data(), n + 1);
+  c.sync();
+  build_long_rows(c, prp, out.cptr_h, out.blong);
+  c.sync();
+}
+
+void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<int32_t>& bounds, LongRows& L) {
+  std::vector<int32_t> rows, irow, ichunk, srows, sitem0;
+  const size_t nb = bounds.size() - 1;
+  L.ptr_h.assign(nb + 1, 0);
+  L.iptr_h.assign(nb + 1, 0);
+  L.sptr_h.assign(nb + 1, 0);
+  for (size_t g = 0; g < nb; ++g) {
+    L.ptr_h[g] = (int32_t)rows.size();
+    L.iptr_h[g] = (int32_t)irow.size();
+    L.sptr_h[g] = (int32_t)srows.size();
+    for (int32_t i = bounds[g]; i < bounds[g + 1]; ++i) {
+      const int64_t len = rp[i + 1] - rp[i];
+      if (len <= kLongRow) continue;
+      if (len <= kChunk) {
+        rows.push_back(i);
+      } else {
+        srows.push_back(i);
+        sitem0.push_back((int32_t)irow.size());
+        for (int64_t q = 0; q * kChunk < len; ++q) {
+          irow.push_back(i);
+          ichunk.push_back((int32_t)q);
+        }
+      }
+    }
+  }
+  L.ptr_h[nb] = (int32_t)rows.size();
+  L.iptr_h[nb] = (int32_t)irow.size();
+  L.sptr_h[nb] = (int32_t)srows.size();
+  sitem0.push_back((int32_t)irow.size());
+  auto up = [&](DVec<int32_t>& d, const std::vector<int32_t>& h) {
+    d.alloc(std::max<size_t>(h.size(), 1), c.s);
+    if (!h.empty()) d.upload(h.data(), (int64_t)h.size());
+  };
+  up(L.rows, rows);
+  up(L.item_row, irow);
+  up(L.item_chunk, ichunk);
+  up(L.srows, srows);
+  up(L.sitem0, sitem0);
+  c.sync();
 }
 
 // One colour: rows [i0, i1) of the permuted operator update in parallel.
@@ -449,6 +496,10 @@ void prepare_throughput(Ctx& c, DHier& h) {
       L.color = std::move(col);
     }
     if (L.direct) build_direct_inverse(c, *L.direct);
+    std::vector<int64_t> nrp((size_t)L.op.n + 1);
+    L.op.rp.download(nrp.data(), L.op.n + 1);
+    c.sync();
+    build_long_rows(c, nrp, std::vector<int32_t>{0, L.op.n}, L.blong_nat);
   }
   c.sync();
 }
