@@ -192,6 +192,16 @@ void lamg_graph_destroy(lamg_graph *g);
 /* builds (once) the throughput-mode colour-permuted copies of the hierarchy */
 int lamg_hier_prepare_throughput(lamg_ctx *ctx, lamg_hier *h);
 
+/* THROUGHPUT smoother of one hierarchy level, for parity tests: the colour
+ * order (row_ids[n]: natural row of each stored row; color_ptr[ncolors+1])
+ * and `sweeps` coloured Gauss-Seidel sweeps on host vectors. nrhs == 1: b, x
+ * are [n]; nrhs in {4,8,16,32}: node-major [n][nrhs]. A coloured sweep is
+ * gauss_seidel_sweep (smoothing.cpp:13-40) in colour-permuted row order. */
+int lamg_hier_color_count(const lamg_hier *h, int32_t level, int32_t *ncolors);
+int lamg_hier_download_colors(const lamg_hier *h, int32_t level, int32_t *row_ids, int32_t *color_ptr);
+int lamg_hier_smooth(lamg_ctx *ctx, const lamg_hier *h, int32_t level, int32_t nrhs, const double *b,
+                     double *x, int32_t sweeps);
+
 /* ---- kernel timing (bench roofline): CUDA events around the finest-level
  * residual and Gauss-Seidel launches of the solves issued on ctx ---------- */
 int lamg_ctx_profile(lamg_ctx *ctx, int enable);

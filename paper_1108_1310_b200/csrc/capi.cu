@@ -575,6 +575,49 @@ int lamg_hier_prepare_throughput(lamg_ctx* ctx, lamg_hier* h) {
   });
 }
 
+static const DColor& color_of(const lamg_hier* h, int32_t l) {
+  const DLevel& L = level_of(h, l);
+  if (!L.color) throw LamgError(LAMG_E_ARGUMENT, "level " + std::to_string(l) + " has no throughput smoother");
+  return *L.color;
+}
+
+int lamg_hier_color_count(const lamg_hier* h, int32_t l, int32_t* ncolors) {
+  return guarded([&] { *ncolors = color_of(h, l).ncolors; });
+}
+
+int lamg_hier_download_colors(const lamg_hier* h, int32_t l, int32_t* row_ids, int32_t* color_ptr) {
+  return guarded([&] {
+    const DColor& cl = color_of(h, l);
+    CK(cudaSetDevice(h->h->device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(row_ids, cl.row_ids.p, sizeof(int32_t) * level_of(h, l).op.n, cudaMemcpyDeviceToHost));
+    memcpy(color_ptr, cl.cptr_h.data(), sizeof(int32_t) * (cl.ncolors + 1));
+  });
+}
+
+int lamg_hier_smooth(lamg_ctx* ctx, const lamg_hier* h, int32_t l, int32_t nrhs, const double* b, double* x,
+                     int32_t sweeps) {
+  return guarded([&] {
+    if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    Ctx& c = ctx->c;
+    set_device(c);
+    const DColor& cl = color_of(h, l);
+    const int64_t len = (int64_t)level_of(h, l).op.n * nrhs;
+    DVec<double> db(len, c.s), dx(len, c.s);
+    db.upload(b, len);
+    dx.upload(x, len);
+    if (nrhs == 1) {
+      gs_colored(c, cl, level_of(h, l).op.n, db.p, dx.p, sweeps);
+    } else {
+      DVec<int32_t> done(nrhs, c.s);
+      done.fill_bytes(0);
+      bgs_colored(c, cl, level_of(h, l).op.n, db.p, dx.p, sweeps, nrhs, done.p);
+    }
+    dx.download(x, len);
+    c.sync();
+  });
+}
+
 // -------------------------------------------------------------- profiling
 int lamg_ctx_profile(lamg_ctx* ctx, int enable) {
   return guarded([&] {
@@ -903,7 +946,10 @@ int lamg_k_coarsest_direct(lamg_ctx* ctx, const lamg_csr* a, const double* b, do
     auto db = up(c, b, a->n);
     auto dx = up(c, x, a->n);
     DVec<double> scratch(2 * (int64_t)d.maxN + 2, c.s);
-    direct_solve(c, d, db.p, dx.p, true, scratch.p);
+    // THROUGHPUT contexts solve with the precomputed inverse, as their solves do
+    const bool exact = c.mode == LAMG_MODE_VALIDATE;
+    if (!exact) build_direct_inverse(c, d);
+    direct_solve(c, d, db.p, dx.p, exact, scratch.p);
     dx.download(x, a->n);
     c.sync();
   });

@@ -93,6 +93,11 @@ enum DevErrKind {
 // that allocated them may belong to a context destroyed in the meantime.
 extern thread_local bool g_free_sync;
 
+inline bool poison_enabled() {
+  static const bool on = getenv("LAMG_POISON") && atoi(getenv("LAMG_POISON")) == 1;
+  return on;
+}
+
 template <typename T>
 struct DVec {
   T* p = nullptr;
@@ -117,6 +122,10 @@ struct DVec {
     s = st;
     n = count;
     if (count > 0) CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, s));
+    // LAMG_POISON=1 (debugging aid): fresh floating-point buffers start as NaN,
+    // so a read of never-written memory shows up in the results
+    if constexpr (std::is_floating_point<T>::value)
+      if (count > 0 && poison_enabled()) CK(cudaMemsetAsync(p, 0xff, sizeof(T) * (size_t)count, s));
   }
   void release() {
     if (p) {

@@ -231,7 +231,25 @@ struct Driver {
   int K = 1;                     // right-hand sides per block (batch.cuh)
   std::vector<int> relax_cols;   // K > 1: relaxation sweeps per column
 
+  // LAMG_TRACE=1 (debugging aid, one column, host-driven levels): norms of b
+  // and x around every level visit
+  double tnorm(const double* v, int64_t n) {
+    double* d = c.dscal + 160;
+    tree_norm2(c, v, n, d);
+    return read_scalar(c, d);
+  }
   void visit(size_t l, const double* b, double* x, int theta) {
+    static const bool trace = getenv("LAMG_TRACE") && atoi(getenv("LAMG_TRACE")) == 1;
+    if (trace && K == 1) {
+      const int64_t n = h.levels[l]->op.n;
+      fprintf(stderr, "[trace] enter l=%zu theta=%d |b|=%.6e |x|=%.6e\n", l, theta, tnorm(b, n), tnorm(x, n));
+      visit_(l, b, x, theta);
+      fprintf(stderr, "[trace] leave l=%zu |x|=%.6e\n", l, tnorm(x, n));
+      return;
+    }
+    visit_(l, b, x, theta);
+  }
+  void visit_(size_t l, const double* b, double* x, int theta) {
     if (!exact && (int)l >= ws.tail.first) {
       ws.tail.run(c, (int)l, theta, cfg.mu, (int)h.levels.size());
       return;
@@ -364,6 +382,8 @@ struct Driver {
     for (int i = 0; i < theta; ++i) {
       if (child.nu_pre) gs(l, b, x, child.nu_pre);
       resid(l, b, x, w.r.p);
+      if (getenv("LAMG_TRACE") && K == 1)
+        fprintf(stderr, "[trace]   l=%zu pre-smoothed |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
       if (adaptive) {
         if (nsaved >= 2) throw LamgError(LAMG_E_ERROR, "recombination supports at most two saved iterates");
         copy_d(c, w.saved_x[nsaved].p, x, L.op.n);
@@ -380,7 +400,15 @@ struct Driver {
       visit(l + 1, wc.b.p, wc.x.p, theta_child);
       if (K > 1) binterpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x, K);
       else interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
+      if (getenv("LAMG_TRACE") && K == 1) {
+        resid(l, b, x, w.r.p);
+        fprintf(stderr, "[trace]   l=%zu corrected |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
+      }
       if (child.nu_post) gs(l, b, x, child.nu_post);
+      if (getenv("LAMG_TRACE") && K == 1) {
+        resid(l, b, x, w.r.p);
+        fprintf(stderr, "[trace]   l=%zu post-smoothed |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
+      }
     }
     if (adaptive && nsaved > 0) {
       recombine(c, L.op.view(), b, nsaved, w, x, exact, growth, &L.sched);

@@ -12,28 +12,77 @@ namespace lamgb {
 
 // First-fit colour in index order: u takes the smallest colour unused by its
 // lower neighbours. Lower neighbours sit in earlier wavefronts, so walking
-// the exact-order fronts reproduces the sequential greedy colouring.
+// the exact-order fronts reproduces the sequential greedy colouring. Rows of
+// one front are independent: short rows take a thread, medium rows a warp
+// and hub rows a whole CTA (power-law levels have hubs with 10^5-10^6 lower
+// neighbours; one thread per hub serialised the colouring for minutes).
+constexpr int64_t kColorWarpRow = 32, kColorBlockRow = 4096;
+
+__device__ __forceinline__ unsigned long long color_window(const CSRv& a, int32_t u, int64_t k0, int64_t step,
+                                                           int32_t base, const int32_t* color) {
+  unsigned long long used = 0ull;
+  for (int64_t k = a.rp[u] + k0; k < a.rp[u + 1]; k += step) {
+    const int32_t v = a.col[k];
+    if (v >= u) break;  // rows are sorted: lower neighbours first
+    const int32_t cv = ((volatile const int32_t*)color)[v] - base;
+    if (cv >= 0 && cv < 64) used |= 1ull << cv;
+  }
+  return used;
+}
+
+__device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
+  const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)v);
+  const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(v >> 32));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
 __global__ void color_fronts_kernel(CSRv a, const int32_t* __restrict__ front_ptr,
                                     const int32_t* __restrict__ rows, int32_t nfronts, int32_t* color) {
+  __shared__ unsigned long long sh_used;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gwarp = gtid >> 5, nwarps = gstride >> 5;
+  const int lane = threadIdx.x & 31;
   for (int32_t f = 0; f < nfronts; ++f) {
-    for (int64_t i = front_ptr[f] + gtid; i < front_ptr[f + 1]; i += gstride) {
+    const int32_t lo = front_ptr[f], hi = front_ptr[f + 1];
+    for (int64_t i = lo + gtid; i < hi; i += gstride) {
       const int32_t u = rows[i];
-      int32_t base = 0;
-      while (true) {
-        unsigned long long used = 0ull;
-        for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k) {
-          int32_t v = a.col[k];
-          if (v >= u) break;  // rows are sorted: lower neighbours first
-          int32_t cv = ((volatile int32_t*)color)[v] - base;
-          if (cv >= 0 && cv < 64) used |= 1ull << cv;
-        }
+      if (a.rp[u + 1] - a.rp[u] > kColorWarpRow) continue;
+      for (int32_t base = 0;; base += 64) {
+        const unsigned long long used = color_window(a, u, 0, 1, base, color);
         if (~used) {
           color[u] = base + __ffsll((long long)~used) - 1;
           break;
         }
-        base += 64;
+      }
+    }
+    for (int64_t i = lo + gwarp; i < hi; i += nwarps) {
+      const int32_t u = rows[i];
+      const int64_t len = a.rp[u + 1] - a.rp[u];
+      if (len <= kColorWarpRow || len > kColorBlockRow) continue;
+      for (int32_t base = 0;; base += 64) {
+        const unsigned long long used = warp_or64(color_window(a, u, lane, 32, base, color));
+        if (~used) {
+          if (lane == 0) color[u] = base + __ffsll((long long)~used) - 1;
+          break;
+        }
+      }
+    }
+    for (int64_t i = lo + blockIdx.x; i < hi; i += gridDim.x) {
+      const int32_t u = rows[i];
+      if (a.rp[u + 1] - a.rp[u] <= kColorBlockRow) continue;
+      for (int32_t base = 0;; base += 64) {
+        if (threadIdx.x == 0) sh_used = 0ull;
+        __syncthreads();
+        const unsigned long long used = warp_or64(color_window(a, u, threadIdx.x, blockDim.x, base, color));
+        if (lane == 0 && used) atomicOr(&sh_used, used);
+        __syncthreads();
+        const unsigned long long all = sh_used;
+        __syncthreads();
+        if (~all) {
+          if (threadIdx.x == 0) color[u] = base + __ffsll((long long)~all) - 1;
+          break;
+        }
       }
     }
     grid_barrier();
@@ -57,17 +106,19 @@ __global__ void perm_deg_kernel(CSRv a, const int32_t* row_ids, int64_t* deg) {
   int32_t u = row_ids[i];
   deg[i] = a.rp[u + 1] - a.rp[u];
 }
+// one warp per stored row (hub rows hold up to 10^6 entries)
 __global__ void perm_fill_kernel(CSRv a, const int32_t* row_ids, const int64_t* prp, int32_t* pcol,
                                  double* pval, double* pdiag) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  int32_t u = row_ids[i];
-  int64_t o = prp[i];
-  for (int64_t k = a.rp[u]; k < a.rp[u + 1]; ++k, ++o) {
-    pcol[o] = a.col[k];
-    pval[o] = a.val[k];
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= a.n) return;
+  const int32_t u = row_ids[w];
+  const int64_t o = prp[w] - a.rp[u];
+  for (int64_t k = a.rp[u] + lane; k < a.rp[u + 1]; k += 32) {
+    pcol[o + k] = a.col[k];
+    pval[o + k] = a.val[k];
   }
-  pdiag[i] = a.diag[u];
+  if (lane == 0) pdiag[w] = a.diag[u];
 }
 
 __global__ void heavy_flags_kernel(const int64_t* rp, int32_t n, uint8_t* f) {
@@ -113,7 +164,7 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   out.col.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
   out.val.alloc(std::max<int64_t>(2 * a.m, 1), c.s);
   out.diag.alloc(n, c.s);
-  count_launch(), perm_fill_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
+  count_launch(), perm_fill_kernel<<<blocks_for((int64_t)n * 32), kThreads, 0, c.s>>>(a, out.row_ids.p, out.rp.p, out.col.p,
                                                                      out.val.p, out.diag.p);
   CK_LAUNCH();
   // heavy rows: per colour (stored positions) and in natural order
@@ -467,7 +518,7 @@ void build_direct_inverse(Ctx& c, DDirect& d) {
   DVec<double> work((int64_t)d.maxN * d.maxN + 1, c.s);
   for (int32_t ci = 0; ci < d.ncomp; ++ci) {
     const int32_t N = d.comp_size[ci] + 1;
-    count_launch(), lu_inverse_kernel<<<blocks_for(N), 128, 0, c.s>>>(d.lu.p + off[ci], d.perm.p + start[ci] + ci, N,
+    count_launch(), lu_inverse_kernel<<<blocks_for(N, 128), 128, 0, c.s>>>(d.lu.p + off[ci], d.perm.p + start[ci] + ci, N,
                                                                    d.inv.p + ioff[ci], work.p);
     CK_LAUNCH();
     c.sync();

@@ -314,6 +314,28 @@ class Hierarchy:
                         d[ps + k] = v
         return d
 
+    def prepare_throughput(self):
+        """Builds the THROUGHPUT smoother data once (colourings, permuted copies)."""
+        _check(self.ctx.lib.lamg_hier_prepare_throughput(self.ctx.p, self.h))
+        self.levels = [self.level_info(l) for l in range(self.nlevels)]
+
+    def colors(self, l: int):
+        """(row_ids, color_ptr) of level l's coloured smoother: stored row -> natural row."""
+        nc = C.c_int32()
+        _check(self.ctx.lib.lamg_hier_color_count(self.h, C.c_int32(l), C.byref(nc)))
+        rows = np.empty(self.levels[l].n, np.int32)
+        ptr = np.empty(nc.value + 1, np.int32)
+        _check(self.ctx.lib.lamg_hier_download_colors(self.h, C.c_int32(l), _p(rows), _p(ptr)))
+        return rows, ptr
+
+    def smooth(self, l: int, b, x, sweeps: int = 1):
+        """`sweeps` THROUGHPUT coloured Gauss-Seidel sweeps on level l; b, x are [n] or node-major [n, K]."""
+        b, x = np.ascontiguousarray(b, np.float64), np.array(x, np.float64, order="C")
+        k = 1 if x.ndim == 1 else x.shape[1]
+        _check(self.ctx.lib.lamg_hier_smooth(self.ctx.p, self.h, C.c_int32(l), C.c_int32(k), _p(b), _p(x),
+                                             C.c_int32(sweeps)))
+        return x
+
     def solve(self, b, x0, **cycle):
         """Oracle-style solve: returns (x, stats dict); errors carry .stats."""
         cfg = CycleConfig(**{k: v for k, v in cycle.items() if k != "seed"})

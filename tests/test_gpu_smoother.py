@@ -1,0 +1,128 @@
+"""THROUGHPUT-mode smoother parity (GPU).
+
+The coloured Gauss-Seidel sweep is gauss_seidel_sweep (smoothing.cpp:13-40)
+run in colour-permuted row order. For every smoothing level of a hierarchy:
+  * the colouring is proper (no edge inside a colour) and, on small levels,
+    equals the sequential first-fit colouring in index order;
+  * one GPU sweep (one column and a 32-column node-major block) matches a
+    scipy restatement of the sequential sweep in the same row order within
+    1e-12 relative (row dot products are summed in a fixed tree, not in
+    column order, so this is a tolerance, not bit parity);
+  * a sweep never raises the energy 1/2 x'Ax - b'x (GS on an SPD-on-range
+    operator is monotone for any row order).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_1108_1310_b200 import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+GRAPHS = {
+    "grid5_64": lambda: G.grid_5pt(64),
+    "grid3d_24": lambda: G.grid3d_7pt(24),
+    "rgg_16k": lambda: G.rgg(1 << 14, seed=3),
+    "rgg_256k": lambda: G.rgg(1 << 18, seed=3),
+    "chunglu_16k": lambda: G.chung_lu(1 << 14, seed=4),
+    "rmat_13": lambda: G.rmat(13, seed=5),
+}
+
+
+def _offdiag(a):
+    return sp.csr_matrix((a.val, a.col, a.row_ptr), shape=(a.n, a.n))
+
+
+def _sweep(A, diag, rows, ptr, b, x):
+    x = x.copy()
+    for c in range(len(ptr) - 1):
+        r = rows[ptr[c]:ptr[c + 1]]
+        r = r[diag[r] != 0.0]  # isolated rows are skipped (smoothing.cpp:20-23)
+        d = diag[r] if x.ndim == 1 else diag[r][:, None]
+        x[r] = (b[r] - A[r] @ x) / d
+    return x
+
+
+def _energy(A, diag, b, x):
+    ax = A @ x + diag * x
+    return 0.5 * float(x @ ax) - float(b @ x)
+
+
+def _greedy(a):
+    color = np.full(a.n, -1, np.int64)
+    for u in range(a.n):
+        nb = a.col[a.row_ptr[u]:a.row_ptr[u + 1]]
+        used = set(color[nb[nb < u]].tolist())
+        c = 0
+        while c in used:
+            c += 1
+        color[u] = c
+    return color
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1108_1310_b200 import lamg as L
+    c = L.Context(0, L.MODE_THROUGHPUT)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name", list(GRAPHS))
+def test_colored_sweep_matches_sequential_restatement(name, ctx):
+    from paper_1108_1310_b200 import lamg as L
+    a = GRAPHS[name]()
+    h = L.setup(a, ctx=ctx)
+    h.prepare_throughput()
+    rng = np.random.default_rng(11)
+    checked = 0
+    for l, li in enumerate(h.levels):
+        if li.colors == 0:
+            continue
+        op = h.op(l)
+        A = _offdiag(op)
+        rows, ptr = h.colors(l)
+        assert ptr[0] == 0 and ptr[-1] == op.n and np.all(np.diff(ptr) >= 0)
+        assert np.array_equal(np.sort(rows), np.arange(op.n))
+        color = np.empty(op.n, np.int64)
+        for c in range(len(ptr) - 1):
+            color[rows[ptr[c]:ptr[c + 1]]] = c
+        u = np.repeat(np.arange(op.n), np.diff(op.row_ptr))
+        assert not np.any(color[u] == color[op.col]), f"level {l}: improper colouring"
+        if op.n <= 70000:
+            assert np.array_equal(color, _greedy(op)), f"level {l}: not the index-order greedy colouring"
+        b = rng.standard_normal(op.n)
+        b -= b.mean()
+        x = rng.standard_normal(op.n)
+        want = _sweep(A, op.diag, rows, ptr, b, x)
+        got = h.smooth(l, b, x, 1)
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err <= 1e-12, f"level {l} (n={op.n}, colours {li.colors}): rel err {err:.3e}"
+        assert _energy(A, op.diag, b, got) <= _energy(A, op.diag, b, x) * (1 - 1e-14) + 1e-9
+        K = 32
+        B = rng.standard_normal((op.n, K))
+        B -= B.mean(axis=0)
+        X = rng.standard_normal((op.n, K))
+        want = _sweep(A, op.diag, rows, ptr, B, X)
+        got = h.smooth(l, B, X, 1)
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err <= 1e-12, f"level {l} block: rel err {err:.3e}"
+        checked += 1
+    assert checked > 0
+
+
+@pytest.mark.parametrize("n", [100, 128, 129, 140, 150])
+def test_throughput_coarsest_inverse(n, ctx):
+    """DirectSolver (coarse_solver.cpp:26-76) through the THROUGHPUT inverse:
+    every inverse column is built (sizes straddling the 128-thread block)."""
+    from oracle import Oracle
+    from paper_1108_1310_b200.lamg import Kernels
+    gpu = Kernels(ctx)
+    port = Oracle("port")
+    for seed in (1, 2):
+        a = G.random_connected(n, 1.2, 700 + seed + n)
+        b = G.random_vector(n, seed, True)
+        x = gpu.coarsest_direct(a, b)
+        want = port.coarsest_direct(a, b)
+        assert np.all(np.isfinite(x))
+        assert np.linalg.norm(x - want) <= 1e-10 * np.linalg.norm(want)
