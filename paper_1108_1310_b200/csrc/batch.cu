@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp
 }
 
 // Long rows (more than kLongRow entries): one CTA per row -- or per chunk of
-// kChunk entries for the longest -- folds 32 strided slices of the entries
+// L.chunk entries for the longest -- folds 32 strided slices of the entries
 // for all K columns; slice partials combine in slice order, chunk sums in
 // chunk order. The order depends on the row only, never on K.
 constexpr int kSL = 32;
@@ -168,11 +168,11 @@ __global__ void __launch_bounds__(kBT) blong_part_kernel(const int64_t* __restri
                                                          const double* __restrict__ val,
                                                          const int32_t* __restrict__ item_row,
                                                          const int32_t* __restrict__ item_chunk, int32_t it0,
-                                                         const double* X, double* scratch) {
+                                                         int64_t chunk, const double* X, double* scratch) {
   const int32_t it = it0 + blockIdx.x;
   const int32_t i = item_row[it];
-  const int64_t cb = rp[i] + (int64_t)item_chunk[it] * kChunk;
-  const int64_t ce = cb + kChunk < rp[i + 1] ? cb + kChunk : rp[i + 1];
+  const int64_t cb = rp[i] + (int64_t)item_chunk[it] * chunk;
+  const int64_t ce = cb + chunk < rp[i + 1] ? cb + chunk : rp[i + 1];
   const double t = long_chunk_dot<K>(col, val, X, cb, ce);
   if ((int)threadIdx.x < K) scratch[(int64_t)it * K + threadIdx.x] = t;
 }
@@ -420,7 +420,7 @@ void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X
         const int32_t ni = L.iptr_h[cc + 1] - L.iptr_h[cc];
         if (ni) {
           count_launch(), blong_part_kernel<KK><<<ni, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, L.item_row.p,
-                                                                    L.item_chunk.p, L.iptr_h[cc], X, scratch);
+                                                                    L.item_chunk.p, L.iptr_h[cc], L.chunk, X, scratch);
           const int32_t ns = L.sptr_h[cc + 1] - L.sptr_h[cc];
           count_launch(), blong_fin_kernel<KK, false><<<bblocks((int64_t)ns * KK), kBT, 0, c.s>>>(
               L.srows.p, L.sitem0.p, L.sptr_h[cc], ns, scratch, cl.row_ids.p, cl.diag.p, B, X, nullptr, done);
@@ -442,7 +442,7 @@ void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const 
     const int32_t ni = L.iptr_h[1];
     if (ni) {
       count_launch(), blong_part_kernel<KK><<<ni, kBT, 0, c.s>>>(a.rp, a.col, a.val, L.item_row.p, L.item_chunk.p, 0,
-                                                                X, scratch);
+                                                                L.chunk, X, scratch);
       const int32_t ns = L.sptr_h[1];
       count_launch(), blong_fin_kernel<KK, true><<<bblocks((int64_t)ns * KK), kBT, 0, c.s>>>(
           L.srows.p, L.sitem0.p, 0, ns, scratch, nullptr, a.diag, B, const_cast<double*>(X), R, nullptr);

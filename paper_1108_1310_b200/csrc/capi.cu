@@ -288,6 +288,9 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   delete c.bws;
   c.bws = nullptr;
   c.bscratch.release();
+  c.rpart.release();
+  c.ripart.release();
+  c.rcptr.release();
   c.res_csr = DCSR();
   c.res_stage.f_diag.release();
   c.res_stage.f_ptr.release();
@@ -964,7 +967,7 @@ int lamg_k_coarsest_relax(lamg_ctx* ctx, const lamg_csr* a, const double* b, dou
     auto dx = up(c, x, a->n);
     DVec<double> r;
     int sw = 0;
-    relax_solve(c, av, sch, nullptr, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
+    relax_solve(c, av, sch, nullptr, nullptr, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
     dx.download(x, a->n);
     c.sync();
   });

@@ -209,6 +209,8 @@ struct Ctx {
   double* dbscal = nullptr;     // batched scalars (256 doubles)
   int32_t* dbdone = nullptr;    // batched per-column masks (64 ints)
   DVec<double> bscratch;        // batched long-row chunk sums (grown on demand)
+  DVec<double> rpart, ripart;   // cooperative relaxation: block partials, chunk partials
+  DVec<int32_t> rcptr;          // cooperative relaxation: natural-order range {0, n}
   // per-kernel API results kept until taken
   DCSR res_csr;
   struct {
@@ -249,6 +251,12 @@ inline int blocks_for(int64_t n, int threads = kThreads) {
   if (b < 1) b = 1;
   if (b > (1 << 30)) b = 1 << 30;
   return (int)b;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 // grid barrier usable from cooperative kernels; one block uses __syncthreads
@@ -324,8 +332,22 @@ __device__ __forceinline__ double group_dot(const int32_t* __restrict__ col, con
 __device__ __forceinline__ double block_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
                                             const double* x, int64_t b, int64_t e) {
   __shared__ double sh_bd[33];
+  constexpr int U = 4;  // loads batched ahead of use: U gathers in flight per thread
   double p = 0.0;
-  for (int64_t k = b + threadIdx.x; k < e; k += blockDim.x) p += __ldcs(val + k) * x[__ldcs(col + k)];
+  for (int64_t k0 = b + threadIdx.x; k0 < e; k0 += (int64_t)blockDim.x * U) {
+    int32_t c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t k = k0 + (int64_t)j * blockDim.x;
+      c[j] = k < e ? __ldcs(col + k) : 0;
+      v[j] = k < e ? __ldcs(val + k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = (k0 + (int64_t)j * blockDim.x < e) ? x[c[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) p += v[j] * xv[j];
+  }
   for (int o = 16; o > 0; o >>= 1) p += __shfl_down_sync(0xffffffffu, p, o);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) sh_bd[threadIdx.x >> 5] = p;

@@ -58,16 +58,22 @@ struct DDirect {
   DVec<int64_t> inv_off;           // [ncomp] offsets into inv
 };
 
-// blocks of K columns (batch.cu): rows longer than kLongRow are reduced by
-// a CTA in 32 strided slices; rows longer than kChunk are split into chunks
-// of kChunk entries (one CTA each) whose sums combine in chunk order
+// Long rows (power-law hubs and their elimination fill): rows longer than
+// kLongRow are reduced by a whole CTA (K columns: 32 strided slices); rows
+// longer than `chunk` entries are split into chunks of `chunk` entries, one
+// CTA each, whose sums combine in chunk order (a fixed order that depends on
+// the row only: never on K, never on which CTA finishes last).
 struct LongRows {
-  DVec<int32_t> rows;                  // long rows (> kLongRow entries, <= kChunk)
+  int64_t chunk = 1024;                // entries per chunk of a super-long row
+  DVec<int32_t> rows;                  // long rows (> kLongRow entries, <= chunk)
   std::vector<int32_t> ptr_h;          // per colour (stored order) or [0, count] (natural)
   DVec<int32_t> item_row, item_chunk;  // super-long rows: (row, chunk) work items
+  DVec<int32_t> item_srow;             // super-long row index of each item
   std::vector<int32_t> iptr_h;
   DVec<int32_t> srows, sitem0;         // super-long rows and their first item
   std::vector<int32_t> sptr_h;
+  DVec<int32_t> ptr_d, iptr_d;         // device copies of ptr_h / iptr_h (persistent kernels)
+  DVec<uint32_t> cnt;                  // per super-long row: chunks finished (mod #chunks)
 };
 // lists over the row ranges `bounds` of a CSR with host row pointers rp
 void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<int32_t>& bounds, LongRows& L);
@@ -95,7 +101,6 @@ struct DColor {
   LongRows blong;  // stored (colour) order, ranges per colour
 };
 constexpr int64_t kLongRow = 64;
-constexpr int64_t kChunk = 16384;
 
 constexpr int64_t kHeavyRow = 2048;
 
@@ -182,8 +187,9 @@ void galerkin(Ctx& c, const CSRv& a, const int32_t* agg, int32_t coarse_n, DCSR&
 void make_direct(Ctx& c, const CSRv& a, DDirect& d);
 // scratch: 2*maxN + 2 doubles
 void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exact, double* scratch);
-void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const double* b,
-                 double* x, DVec<double>& r, int* sweeps_out, bool exact);
+// col/nat: the THROUGHPUT colouring and natural-order long-row lists (nullptr: VALIDATE path)
+void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const LongRows* nat,
+                 const double* b, double* x, DVec<double>& r, int* sweeps_out, bool exact);
 
 // throughput mode (throughput.cu)
 void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out);
@@ -196,7 +202,8 @@ inline int row_group_for(int64_t n, int64_t m) {
 }
 void build_direct_inverse(Ctx& c, DDirect& d);
 // whole relaxation-coarsest solve in one cooperative launch; returns sweeps
-int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const double* b, double* x, double* r);
+int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
+                       double* r);
 void prepare_throughput(Ctx& c, DHier& h);
 
 }  // namespace lamgb

@@ -1131,11 +1131,11 @@ void direct_solve(Ctx& c, const DDirect& d, const double* b, double* x, bool exa
 
 // RelaxationSolver::solve (coarse_solver.cpp:82-93); validate mode: exact-order
 // sweeps and sequential folds, one host check per sweep
-void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const double* b,
-                 double* x, DVec<double>& r, int* sweeps_out, bool exact) {
+void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, const LongRows* nat,
+                 const double* b, double* x, DVec<double>& r, int* sweeps_out, bool exact) {
   if (r.n < a.n) r.alloc(a.n, c.s);
-  if (!exact && col) {
-    const int sw = relax_colored_coop(c, a, *col, b, x, r.p);
+  if (!exact && col && nat) {
+    const int sw = relax_colored_coop(c, a, *col, *nat, b, x, r.p);
     c.work += (double)a.m * (1.0 + 2.0 * sw);
     *sweeps_out = sw;
     return;

@@ -281,7 +281,7 @@ struct Driver {
       direct_solve(c, *L.direct, b, x, exact, ws.direct_scratch.p);
     } else {
       int sw = 0;
-      relax_solve(c, L.op.view(), L.sched, L.color.get(), b, x, ws.lv[l].r, &sw, exact);
+      relax_solve(c, L.op.view(), L.sched, L.color.get(), &L.blong_nat, b, x, ws.lv[l].r, &sw, exact);
       relax_sweeps += sw;
     }
   }

@@ -6,6 +6,8 @@
 // change.
 #include <algorithm>
 
+#include <cuda/atomic>
+
 #include "hier.cuh"
 
 namespace lamgb {
@@ -198,7 +200,12 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
 }
 
 void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<int32_t>& bounds, LongRows& L) {
-  std::vector<int32_t> rows, irow, ichunk, srows, sitem0;
+  static const int64_t chunk = [] {
+    const char* e = getenv("LAMG_CHUNK");
+    return e ? std::max<int64_t>(256, atoll(e)) : (int64_t)1024;
+  }();
+  L.chunk = chunk;
+  std::vector<int32_t> rows, irow, ichunk, isrow, srows, sitem0;
   const size_t nb = bounds.size() - 1;
   L.ptr_h.assign(nb + 1, 0);
   L.iptr_h.assign(nb + 1, 0);
@@ -210,15 +217,16 @@ void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<i
     for (int32_t i = bounds[g]; i < bounds[g + 1]; ++i) {
       const int64_t len = rp[i + 1] - rp[i];
       if (len <= kLongRow) continue;
-      if (len <= kChunk) {
+      if (len <= chunk) {
         rows.push_back(i);
       } else {
-        srows.push_back(i);
         sitem0.push_back((int32_t)irow.size());
-        for (int64_t q = 0; q * kChunk < len; ++q) {
+        for (int64_t q = 0; q * chunk < len; ++q) {
           irow.push_back(i);
           ichunk.push_back((int32_t)q);
+          isrow.push_back((int32_t)srows.size());
         }
+        srows.push_back(i);
       }
     }
   }
@@ -233,8 +241,13 @@ void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<i
   up(L.rows, rows);
   up(L.item_row, irow);
   up(L.item_chunk, ichunk);
+  up(L.item_srow, isrow);
   up(L.srows, srows);
   up(L.sitem0, sitem0);
+  up(L.ptr_d, L.ptr_h);
+  up(L.iptr_d, L.iptr_h);
+  L.cnt.alloc(std::max<size_t>(srows.size(), 1), c.s);
+  L.cnt.zero();
   c.sync();
 }
 
@@ -361,127 +374,358 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
 
 // RelaxationSolver::solve (coarse_solver.cpp:82-93) for THROUGHPUT mode in
 // ONE cooperative launch: coloured sweeps separated by grid barriers, fixed-
-// order tree reductions (block partials summed in block order by every
-// thread), the convergence test on the device. Power-law hierarchies end in a
-// multi-million-row relaxation coarsest with hundreds of colours; host-driven
-// that is a launch per colour plus a host round trip per sweep.
-template <int G>
-__device__ inline void coop_residual(const CSRv& a, const double* __restrict__ b, const double* x, double* r,
-                                     const int32_t* heavy_nat, int32_t nheavy) {
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int32_t h = blockIdx.x; h < nheavy; h += gridDim.x) {
-    const int32_t u = heavy_nat[h];
-    const double dot = block_dot(a.col, a.val, x, a.rp[u], a.rp[u + 1]);
-    if (threadIdx.x == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
-  }
-  const int64_t span = ((int64_t)a.n * G + 31) / 32 * 32;
-  for (int64_t t = gtid; t < span; t += gstride) {
-    const int64_t u = t / G;
-    const bool ok = u < a.n && a.rp[u + 1] - a.rp[u] <= kHeavyRow;
-    const double dot = group_dot<G, true>(a.col, a.val, x, ok ? a.rp[u] : 0, ok ? a.rp[u + 1] : 0);
-    if (ok && (threadIdx.x & (G - 1)) == 0) r[u] = b[u] - (a.diag[u] * x[u] + dot);
+// order tree reductions, the convergence test on the device. Power-law
+// hierarchies end in a multi-million-row relaxation coarsest with hundreds of
+// colours and hub rows of 10^5 entries; host-driven that is a launch per
+// colour plus a host round trip per sweep.
+//
+// Work per colour (and per residual) is a list of CTA tasks sized so that no
+// task serialises a hub: chunk items of super-long rows (L.chunk entries,
+// one CTA each), long rows (kLongRow < len <= chunk, a warp each, 8 per
+// task), and blocks of short rows (G lanes per row). A super-long row's
+// chunk partials are summed in chunk order -- in a GS phase by the CTA that
+// finishes the row's last chunk (acquire/release counter), in a residual
+// after the phase barrier. The high colours of a power-law level hold only a
+// few hub rows, so a phase is one chunk task long: each CTA loads its first
+// task's entries of the next phase BEFORE the barrier; after the barrier
+// only the x gathers remain on the critical path.
+struct RelaxOp {
+  const int64_t* rp;  // [n+1] (stored order for the coloured operator)
+  const int32_t* col;
+  const double* val;
+  const double* diag;     // diag of each stored row
+  const int32_t* row_ids; // stored row -> natural row (nullptr: identity)
+  const int32_t* cptr;    // [ncolors+1] colour ranges (natural operator: {0, n})
+  int32_t ncolors;
+  // LongRows lists (per colour)
+  const int32_t* lrows;
+  const int32_t* lptr;
+  const int32_t* item_row;
+  const int32_t* item_chunk;
+  const int32_t* item_srow;
+  const int32_t* iptr;
+  const int32_t* sitem0;
+  const int32_t* srows;
+  int32_t nsrows;
+  uint32_t* cnt;
+  double* ipart;  // per item partial sums
+  int64_t chunk;
+};
+
+constexpr int kRT = 256;   // threads per CTA of the cooperative relaxation
+constexpr int kRU = 4;     // entries per thread per round of a chunk task
+
+// a CTA's prefetched first chunk task of a phase (registers, per thread)
+struct ChunkPre {
+  int64_t t = -1;  // task index in the phase (-1: none)
+  int64_t ce = 0;
+  int32_t c[kRU];
+  double v[kRU];
+};
+
+__device__ __forceinline__ void chunk_bounds(const RelaxOp& o, int32_t it, int32_t* i, int64_t* cb, int64_t* ce) {
+  *i = o.item_row[it];
+  *cb = o.rp[*i] + (int64_t)o.item_chunk[it] * o.chunk;
+  const int64_t e = o.rp[*i + 1];
+  *ce = *cb + o.chunk < e ? *cb + o.chunk : e;
+}
+
+__device__ __forceinline__ void chunk_load(const RelaxOp& o, int64_t k0, int64_t ce, ChunkPre& p) {
+#pragma unroll
+  for (int j = 0; j < kRU; ++j) {
+    const int64_t k = k0 + (int64_t)j * kRT;
+    p.c[j] = k < ce ? __ldcs(o.col + k) : 0;
+    p.v[j] = k < ce ? __ldcs(o.val + k) : 0.0;
   }
 }
 
+// CTA sum of val*x over [cb, ce) whose first round (entries cb + tid + j*kRT)
+// is already in p; fixed order: strided per thread, warp tree, warps in order
+__device__ __forceinline__ double chunk_dot(const RelaxOp& o, const double* x, int64_t cb, int64_t ce,
+                                            const ChunkPre& p) {
+  __shared__ double sh_cd[kRT / 32 + 1];
+  double acc = 0.0;
+  {
+    double xv[kRU];
+#pragma unroll
+    for (int j = 0; j < kRU; ++j) xv[j] = cb + threadIdx.x + (int64_t)j * kRT < ce ? x[p.c[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kRU; ++j) acc += p.v[j] * xv[j];
+  }
+  for (int64_t k0 = cb + threadIdx.x + (int64_t)kRU * kRT; k0 < ce; k0 += (int64_t)kRU * kRT) {
+    ChunkPre q;
+    chunk_load(o, k0, ce, q);
+    double xv[kRU];
+#pragma unroll
+    for (int j = 0; j < kRU; ++j) xv[j] = k0 + (int64_t)j * kRT < ce ? x[q.c[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kRU; ++j) acc += q.v[j] * xv[j];
+  }
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh_cd[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kRT / 32; ++w) t += sh_cd[w];
+    sh_cd[kRT / 32] = t;
+  }
+  __syncthreads();
+  return sh_cd[kRT / 32];
+}
+
+// GS chunk task: thread 0 of the CTA finishing row s's last chunk gets true
+// and the row's off-diagonal sum (chunk order)
+__device__ __forceinline__ bool chunk_finish(const RelaxOp& o, int32_t it, double p, double* tot) {
+  if (threadIdx.x != 0) return false;
+  o.ipart[it] = p;
+  const int32_t s = o.item_srow[it];
+  const int32_t j0 = o.sitem0[s], j1 = o.sitem0[s + 1];
+  cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cnt(o.cnt[s]);
+  const uint32_t old = cnt.fetch_add(1u, cuda::memory_order_acq_rel);
+  if ((old + 1) % (uint32_t)(j1 - j0) != 0) return false;
+  double t = 0.0;
+  for (int32_t j = j0; j < j1; ++j) t += __ldcg(o.ipart + j);
+  *tot = t;
+  return true;
+}
+
+__device__ __forceinline__ int64_t phase_tasks(const RelaxOp& o, int32_t c, int G, int64_t* nit, int64_t* nlw) {
+  *nit = o.iptr[c + 1] - o.iptr[c];
+  *nlw = (o.lptr[c + 1] - o.lptr[c] + 7) / 8;  // long rows: a warp each, 8 per CTA task
+  const int rpb = kRT / G;
+  return *nit + *nlw + ((int64_t)(o.cptr[c + 1] - o.cptr[c]) + rpb - 1) / rpb;
+}
+
+// loads the first task of this CTA in phase c when it is a chunk item
+__device__ __forceinline__ void phase_prefetch(const RelaxOp& o, int32_t c, int G, int32_t rot, ChunkPre& p) {
+  int64_t nit, nlw;
+  phase_tasks(o, c, G, &nit, &nlw);
+  const int64_t t = ((int64_t)blockIdx.x + rot) % gridDim.x;
+  p.t = -1;
+  if (t < nit) {
+    int32_t i;
+    int64_t cb;
+    chunk_bounds(o, o.iptr[c] + (int32_t)t, &i, &cb, &p.ce);
+    chunk_load(o, cb + threadIdx.x, p.ce, p);
+    p.t = t;
+  }
+}
+
+// One colour c: GS update (x_u = (b_u - dot)/d) or residual (r_u = b_u -
+// (d x_u + dot); super-long rows are left to residual_finish).
+template <int G, bool GS>
+__device__ void relax_phase(const RelaxOp& o, int32_t c, const double* __restrict__ b, double* x, double* r,
+                            int32_t rot, const ChunkPre& pre) {
+  constexpr int RPB = kRT / G;  // short rows per CTA task
+  int64_t nit, nlw;
+  const int64_t T = phase_tasks(o, c, G, &nit, &nlw);
+  const int32_t i0 = o.cptr[c], i1 = o.cptr[c + 1];
+  const int32_t it0 = o.iptr[c];
+  const int32_t l0 = o.lptr[c], nl = o.lptr[c + 1] - l0;
+  const int64_t start = ((int64_t)blockIdx.x + rot) % gridDim.x;
+  for (int64_t t = start; t < T; t += gridDim.x) {
+    if (t < nit) {
+      const int32_t it = it0 + (int32_t)t;
+      int32_t i;
+      int64_t cb, ce;
+      chunk_bounds(o, it, &i, &cb, &ce);
+      double p;
+      if (t == pre.t) {
+        p = chunk_dot(o, x, cb, ce, pre);
+      } else {
+        ChunkPre q;
+        chunk_load(o, cb + threadIdx.x, ce, q);
+        p = chunk_dot(o, x, cb, ce, q);
+      }
+      if (GS) {
+        double dot;
+        if (chunk_finish(o, it, p, &dot)) {
+          const int32_t u = o.row_ids ? o.row_ids[i] : i;
+          x[u] = (b[u] - dot) / o.diag[i];
+        }
+      } else if (threadIdx.x == 0) {
+        o.ipart[it] = p;
+      }
+    } else if (t < nit + nlw) {
+      const int64_t j = (t - nit) * 8 + (threadIdx.x >> 5);
+      const bool ok = j < nl;
+      const int32_t i = ok ? o.lrows[l0 + j] : 0;
+      const double dot = group_dot<32, true>(o.col, o.val, x, ok ? o.rp[i] : 0, ok ? o.rp[i + 1] : 0);
+      if (ok && (threadIdx.x & 31) == 0) {
+        const int32_t u = o.row_ids ? o.row_ids[i] : i;
+        if (GS) x[u] = (b[u] - dot) / o.diag[i];
+        else r[u] = b[u] - (o.diag[i] * x[u] + dot);
+      }
+    } else {
+      const int64_t i = i0 + (t - nit - nlw) * RPB + threadIdx.x / G;
+      const bool ok = i < i1 && o.rp[i + 1] - o.rp[i] <= kLongRow;
+      const double dot = group_dot<G, true>(o.col, o.val, x, ok ? o.rp[i] : 0, ok ? o.rp[i + 1] : 0);
+      if (ok && (threadIdx.x & (G - 1)) == 0) {
+        const int32_t u = o.row_ids ? o.row_ids[i] : (int32_t)i;
+        if (GS) x[u] = (b[u] - dot) / o.diag[i];
+        else r[u] = b[u] - (o.diag[i] * x[u] + dot);
+      }
+    }
+  }
+}
+
+// after the residual phase's barrier: super-long rows of the natural
+// operator from their chunk partials (chunk order); returns this thread's
+// share of sum r^2 over those rows
+__device__ __forceinline__ double residual_finish(const RelaxOp& o, const double* __restrict__ b, const double* x,
+                                                  double* r) {
+  double loc = 0.0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < o.nsrows;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int32_t j = o.sitem0[s]; j < o.sitem0[s + 1]; ++j) t += __ldcg(o.ipart + j);
+    const int32_t u = o.srows[s];
+    const double ru = b[u] - (o.diag[u] * x[u] + t);
+    r[u] = ru;
+    loc += ru * ru;
+  }
+  return loc;
+}
+
+// grid-wide sum: block partials, then every block folds all partials in the
+// same fixed order (strided per thread, then a fixed block tree), so every
+// thread of the grid gets the identical value
 __device__ inline double coop_sum(double v, double* part) {
-  __shared__ double sh[33];
+  __shared__ double sh[kRT];
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    for (int w = 0; w < kRT / 32; ++w) t += sh[w];
     part[blockIdx.x] = t;
   }
   cg::this_grid().sync();
   double t = 0.0;
-  for (unsigned g = 0; g < gridDim.x; ++g) t += ((volatile double*)part)[g];
+  for (unsigned g = threadIdx.x; g < gridDim.x; g += kRT) t += __ldcg(part + g);
+  sh[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = kRT / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  t = sh[0];
   cg::this_grid().sync();
   return t;
 }
 
+// residual of the natural operator and its squared norm (super-long rows
+// finished after the barrier; the sum skips them in the row loop)
 template <int G>
-__global__ void relax_coop_kernel(CSRv a, const int64_t* __restrict__ prp, const int32_t* __restrict__ pcol,
-                                  const double* __restrict__ pval, const double* __restrict__ pdiag,
-                                  const int32_t* __restrict__ row_ids, const int32_t* __restrict__ cptr,
-                                  int32_t ncolors, const int32_t* __restrict__ heavy,
-                                  const int32_t* __restrict__ hptr, const int32_t* __restrict__ heavy_nat,
-                                  int32_t nheavy_nat, const double* __restrict__ b, double* x, double* r,
-                                  double* part, int* sweeps_out) {
+__device__ double relax_residual_norm2(const RelaxOp& no, int32_t n, const double* __restrict__ b, const double* x,
+                                       double* r, double* part) {
+  ChunkPre none;
+  relax_phase<G, false>(no, 0, b, const_cast<double*>(x), r, 0, none);
+  cg::this_grid().sync();
+  double loc = residual_finish(no, b, x, r);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    if (no.rp[u + 1] - no.rp[u] <= no.chunk) loc += r[u] * r[u];
+  return coop_sum(loc, part);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kRT) relax_coop_kernel(RelaxOp po, RelaxOp no, int32_t n,
+                                                         const double* __restrict__ b, double* x, double* r,
+                                                         double* part, int* sweeps_out, uint64_t* tstamp) {
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  coop_residual<G>(a, b, x, r, heavy_nat, nheavy_nat);
-  cg::this_grid().sync();
-  double loc = 0.0;
-  for (int64_t u = gtid; u < a.n; u += gstride) loc += r[u] * r[u];
-  const double r0 = sqrt(coop_sum(loc, part));
+  const double r0 = sqrt(relax_residual_norm2<G>(no, n, b, x, r, part));
   int sweeps = 0;
   if (r0 != 0.0) {
     const double target = 1e-12 * r0;
+    if (tstamp && gtid == 0) tstamp[po.ncolors + 2] = globaltimer_ns();
+    ChunkPre pre;
     for (int sweep = 0; sweep < 400; ++sweep) {
-      for (int32_t cc = 0; cc < ncolors; ++cc) {
-        const int32_t i0 = cptr[cc], i1 = cptr[cc + 1];
-        for (int32_t hh = hptr[cc] + blockIdx.x; hh < hptr[cc + 1]; hh += gridDim.x) {
-          const int32_t i = heavy[hh];
-          const double dot = block_dot(pcol, pval, x, prp[i], prp[i + 1]);
-          if (threadIdx.x == 0) {
-            const int32_t u = row_ids[i];
-            x[u] = (b[u] - dot) / pdiag[i];
-          }
-        }
-        const int64_t span = ((int64_t)(i1 - i0) * G + 31) / 32 * 32;
-        for (int64_t t = gtid; t < span; t += gstride) {
-          const int64_t i = i0 + t / G;
-          const bool ok = i < i1 && prp[i + 1] - prp[i] <= kHeavyRow;
-          const double dot = group_dot<G, true>(pcol, pval, x, ok ? prp[i] : 0, ok ? prp[i + 1] : 0);
-          if (ok && (threadIdx.x & (G - 1)) == 0) {
-            const int32_t u = row_ids[i];
-            x[u] = (b[u] - dot) / pdiag[i];
-          }
-        }
+      int32_t rot = 0;
+      phase_prefetch(po, 0, G, rot, pre);
+      for (int32_t cc = 0; cc < po.ncolors; ++cc) {
+        relax_phase<G, true>(po, cc, b, x, r, rot, pre);
+        // the next phase starts where this one's longest tasks did not
+        rot += (po.iptr[cc + 1] - po.iptr[cc]) + (po.lptr[cc + 1] - po.lptr[cc] + 7) / 8;
+        if (cc + 1 < po.ncolors) phase_prefetch(po, cc + 1, G, rot, pre);
         cg::this_grid().sync();
+        if (tstamp && sweep == 0 && gtid == 0) tstamp[cc] = globaltimer_ns();
       }
-      loc = 0.0;
-      for (int64_t u = gtid; u < a.n; u += gstride) loc += x[u];
-      const double mean = coop_sum(loc, part) / (double)a.n;
-      for (int64_t u = gtid; u < a.n; u += gstride) x[u] = x[u] - mean;
+      if (tstamp && sweep == 0 && gtid == 0) tstamp[po.ncolors] = globaltimer_ns();
+      double loc = 0.0;
+      for (int64_t u = gtid; u < n; u += gstride) loc += x[u];
+      const double mean = coop_sum(loc, part) / (double)n;
+      for (int64_t u = gtid; u < n; u += gstride) x[u] = x[u] - mean;
       cg::this_grid().sync();
-      coop_residual<G>(a, b, x, r, heavy_nat, nheavy_nat);
-      cg::this_grid().sync();
-      loc = 0.0;
-      for (int64_t u = gtid; u < a.n; u += gstride) loc += r[u] * r[u];
+      const double rn = sqrt(relax_residual_norm2<G>(no, n, b, x, r, part));
+      if (tstamp && sweep == 0 && gtid == 0) tstamp[po.ncolors + 1] = globaltimer_ns();
       ++sweeps;
-      if (sqrt(coop_sum(loc, part)) <= target) break;
+      if (rn <= target) break;
     }
   }
   if (gtid == 0) *sweeps_out = sweeps;
 }
 
-int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const double* b, double* x, double* r) {
-  const int threads = 256;
+static RelaxOp relax_op(const int64_t* rp, const int32_t* col, const double* val, const double* diag,
+                        const int32_t* row_ids, const int32_t* cptr, int32_t ncolors, const LongRows& L,
+                        double* ipart) {
+  return RelaxOp{rp, col, val, diag, row_ids, cptr, ncolors, L.rows.p, L.ptr_d.p, L.item_row.p, L.item_chunk.p,
+                 L.item_srow.p, L.iptr_d.p, L.sitem0.p, L.srows.p, L.sptr_h.back(), L.cnt.p, ipart, L.chunk};
+}
+
+int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
+                       double* r) {
+  const int threads = kRT;
   const void* k = cl.group == 8 ? (const void*)relax_coop_kernel<8> : (const void*)relax_coop_kernel<1>;
-  const int blocks = c.max_coop_blocks(k, threads);
-  static thread_local DVec<double> part;
-  if (part.n < blocks || part.s != c.s) part.alloc(blocks, c.s);
+  int blocks = c.max_coop_blocks(k, threads);
+  if (const char* e = getenv("LAMG_RELAX_BLOCKS")) blocks = std::max(1, std::min(blocks, atoi(e)));
+  DVec<double>& part = c.rpart;
+  if (part.n < blocks) part.alloc(blocks, c.s);
+  DVec<double>& ipart = c.ripart;
+  const int64_t nitems = std::max<int64_t>(1, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back());
+  if (ipart.n < nitems) ipart.alloc(nitems, c.s);
+  DVec<int32_t>& nat_cptr = c.rcptr;
+  if (nat_cptr.n < 2) nat_cptr.alloc(2, c.s);
+  const int32_t ncp[2] = {0, a.n};
+  nat_cptr.upload(ncp, 2);
   int* sw = c.dflag + 30;
-  CSRv av = a;
-  const int64_t* prp = cl.rp.p;
-  const int32_t* pcol = cl.col.p;
-  const double* pval = cl.val.p;
-  const double* pdiag = cl.diag.p;
-  const int32_t* rid = cl.row_ids.p;
-  const int32_t* cptr = (const int32_t*)(cl.rp.p + a.n + 1);
-  int32_t nc = cl.ncolors;
+  RelaxOp po = relax_op(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, (const int32_t*)(cl.rp.p + a.n + 1),
+                        cl.ncolors, cl.blong, ipart.p);
+  RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, nat_cptr.p, 1, nat,
+                        ipart.p + cl.blong.iptr_h.back());
+  int32_t n = a.n;
   double* pp = part.p;
-  const int32_t* hv = cl.heavy.p;
-  const int32_t* hp = cl.hptr.p;
-  const int32_t* hn = cl.heavy_nat.p;
-  int32_t nhn = cl.nheavy_nat;
-  void* args[] = {&av, (void*)&prp, (void*)&pcol, (void*)&pval, (void*)&pdiag, (void*)&rid, (void*)&cptr, &nc,
-                  (void*)&hv, (void*)&hp, (void*)&hn, &nhn, (void*)&b, &x, &r, &pp, &sw};
+  // LAMG_RELAX_TIMING=1 (diagnostic): device timestamps of the first sweep's
+  // colour phases, printed as a summary on stderr
+  static const bool timing = getenv("LAMG_RELAX_TIMING") && atoi(getenv("LAMG_RELAX_TIMING")) == 1;
+  DVec<uint64_t> ts;
+  uint64_t* tsp = nullptr;
+  if (timing) {
+    ts.alloc(cl.ncolors + 3, c.s);
+    ts.zero();
+    tsp = ts.p;
+  }
+  void* args[] = {&po, &no, &n, (void*)&b, &x, &r, &pp, &sw, &tsp};
   coop_launch(c, k, blocks, threads, args);
-  return read_i32(c, sw);
+  const int sweeps = read_i32(c, sw);
+  if (timing) {
+    std::vector<uint64_t> t = ts.to_host();
+    const int nc = cl.ncolors;
+    std::vector<double> d(nc);
+    for (int i = 0; i < nc; ++i) d[i] = (double)(t[i] - (i ? t[i - 1] : t[nc + 2])) * 1e-3;
+    std::vector<double> sd = d;
+    std::sort(sd.begin(), sd.end());
+    double tot = 0.0;
+    for (double v : d) tot += v;
+    fprintf(stderr, "[relax timing] blocks %d colours %d: GS phases total %.1f us (min %.2f med %.2f max %.2f), "
+            "mean+residual %.1f us; items %d long rows %d\n", blocks, nc, tot, sd[0], sd[nc / 2], sd[nc - 1],
+            (double)(t[nc + 1] - t[nc - 1]) * 1e-3, cl.blong.iptr_h.back(), cl.blong.ptr_h.back());
+    for (int i = 0; i < nc; i += std::max(1, nc / 16))
+      fprintf(stderr, "  colour %d: %.2f us rows %d items %d long %d\n", i, d[i], cl.cptr_h[i + 1] - cl.cptr_h[i],
+              cl.blong.iptr_h[i + 1] - cl.blong.iptr_h[i], cl.blong.ptr_h[i + 1] - cl.blong.ptr_h[i]);
+  }
+  return sweeps;
 }
 
 // Rows [0, cn) of the inverse of each bordered LU factor: x = Minv[:cn,:cn] b
