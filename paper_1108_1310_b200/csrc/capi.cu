@@ -967,7 +967,15 @@ int lamg_k_coarsest_relax(lamg_ctx* ctx, const lamg_csr* a, const double* b, dou
     auto dx = up(c, x, a->n);
     DVec<double> r;
     int sw = 0;
-    relax_solve(c, av, sch, nullptr, nullptr, db.p, dx.p, r, &sw, c.mode == LAMG_MODE_VALIDATE);
+    const bool exact = c.mode == LAMG_MODE_VALIDATE;
+    // THROUGHPUT contexts run the coloured relaxation their solves use
+    std::unique_ptr<DColor> col;
+    LongRows nat;
+    if (!exact) {
+      col = make_color(c, av, sch);
+      build_natural_long_rows(c, av, nat);
+    }
+    relax_solve(c, av, sch, col.get(), exact ? nullptr : &nat, db.p, dx.p, r, &sw, exact);
     dx.download(x, a->n);
     c.sync();
   });

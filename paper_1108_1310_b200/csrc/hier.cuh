@@ -99,6 +99,20 @@ struct DColor {
   DVec<int32_t> heavy_nat;      // natural rows with more than kHeavyRow entries
   int32_t nheavy_nat = 0;
   LongRows blong;  // stored (colour) order, ranges per colour
+  // relaxation-coarsest sweep as a CUDA graph (relax_colored_graph), per
+  // (b, x, r) buffer set
+  struct SweepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void *b = nullptr, *x = nullptr, *r = nullptr;
+    long long launches = 0;
+  };
+  mutable SweepGraph sweep_graph;
+  DColor() = default;
+  DColor(const DColor&) = delete;
+  DColor& operator=(const DColor&) = delete;
+  ~DColor() {
+    if (sweep_graph.exec) cudaGraphExecDestroy(sweep_graph.exec);
+  }
 };
 constexpr int64_t kLongRow = 64;
 
@@ -204,6 +218,12 @@ void build_direct_inverse(Ctx& c, DDirect& d);
 // whole relaxation-coarsest solve in one cooperative launch; returns sweeps
 int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
                        double* r);
+// the same as a per-sweep CUDA graph of task launches (large levels)
+int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
+                        double* r);
 void prepare_throughput(Ctx& c, DHier& h);
+// THROUGHPUT smoother data of one operator (colouring + colour-permuted copy)
+std::unique_ptr<DColor> make_color(Ctx& c, const CSRv& a, const Schedule& sch);
+void build_natural_long_rows(Ctx& c, const CSRv& a, LongRows& out);
 
 }  // namespace lamgb

@@ -1135,7 +1135,11 @@ void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, 
                  const double* b, double* x, DVec<double>& r, int* sweeps_out, bool exact) {
   if (r.n < a.n) r.alloc(a.n, c.s);
   if (!exact && col && nat) {
-    const int sw = relax_colored_coop(c, a, *col, *nat, b, x, r.p);
+    // LAMG_RELAX_PATH=coop|graph overrides the size rule
+    const char* path = getenv("LAMG_RELAX_PATH");
+    const bool graph = path ? std::string(path) == "graph" : a.n >= (1 << 20);
+    const int sw = graph ? relax_colored_graph(c, a, *col, *nat, b, x, r.p)
+                         : relax_colored_coop(c, a, *col, *nat, b, x, r.p);
     c.work += (double)a.m * (1.0 + 2.0 * sw);
     *sweeps_out = sw;
     return;

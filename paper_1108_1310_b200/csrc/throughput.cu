@@ -636,6 +636,7 @@ __global__ void __launch_bounds__(kRT) relax_coop_kernel(RelaxOp po, RelaxOp no,
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const double r0 = sqrt(relax_residual_norm2<G>(no, n, b, x, r, part));
+  if (tstamp && gtid == 0) reinterpret_cast<double*>(tstamp)[po.ncolors + 3 + 64] = r0;
   int sweeps = 0;
   if (r0 != 0.0) {
     const double target = 1e-12 * r0;
@@ -660,6 +661,7 @@ __global__ void __launch_bounds__(kRT) relax_coop_kernel(RelaxOp po, RelaxOp no,
       cg::this_grid().sync();
       const double rn = sqrt(relax_residual_norm2<G>(no, n, b, x, r, part));
       if (tstamp && sweep == 0 && gtid == 0) tstamp[po.ncolors + 1] = globaltimer_ns();
+      if (tstamp && sweep < 64 && gtid == 0) reinterpret_cast<double*>(tstamp)[po.ncolors + 3 + sweep] = rn;
       ++sweeps;
       if (rn <= target) break;
     }
@@ -672,6 +674,111 @@ static RelaxOp relax_op(const int64_t* rp, const int32_t* col, const double* val
                         double* ipart) {
   return RelaxOp{rp, col, val, diag, row_ids, cptr, ncolors, L.rows.p, L.ptr_d.p, L.item_row.p, L.item_chunk.p,
                  L.item_srow.p, L.iptr_d.p, L.sitem0.p, L.srows.p, L.sptr_h.back(), L.cnt.p, ipart, L.chunk};
+}
+
+// One launch per colour (and per residual): a CTA per task, so the hardware
+// scheduler keeps every SM full with short tasks at full occupancy instead of
+// a co-resident grid walking its task list serially.
+template <int G, bool GS>
+__global__ void __launch_bounds__(kRT) relax_task_kernel(RelaxOp o, int32_t c, const double* __restrict__ b,
+                                                         double* x, double* r) {
+  ChunkPre none;
+  relax_phase<G, GS>(o, c, b, x, r, 0, none);
+}
+__global__ void relax_resfin_kernel(RelaxOp no, const double* __restrict__ b, const double* x, double* r) {
+  residual_finish(no, b, x, r);
+}
+
+static int64_t phase_tasks_h(const std::vector<int32_t>& cptr, const LongRows& L, int32_t c, int G) {
+  const int rpb = kRT / G;
+  return (int64_t)(L.iptr_h[c + 1] - L.iptr_h[c]) + (L.ptr_h[c + 1] - L.ptr_h[c] + 7) / 8 +
+         ((int64_t)(cptr[c + 1] - cptr[c]) + rpb - 1) / rpb;
+}
+
+// RelaxationSolver::solve (coarse_solver.cpp:82-93), THROUGHPUT, for large
+// relaxation-coarsest levels: per sweep one CUDA graph (a task launch per
+// colour, mean subtraction, residual, norm), the convergence test on the
+// host after each sweep (one 8-byte read; a sweep is milliseconds here).
+int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
+                        double* r) {
+  const int G = cl.group == 8 ? 8 : 1;
+  DVec<double>& ipart = c.ripart;
+  const int64_t nitems = std::max<int64_t>(1, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back());
+  if (ipart.n < nitems) ipart.alloc(nitems, c.s);
+  DVec<int32_t>& nat_cptr = c.rcptr;
+  if (nat_cptr.n < 2) nat_cptr.alloc(2, c.s);
+  const int32_t ncp[2] = {0, a.n};
+  nat_cptr.upload(ncp, 2);
+  const RelaxOp po = relax_op(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
+                              (const int32_t*)(cl.rp.p + a.n + 1), cl.ncolors, cl.blong, ipart.p);
+  const RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, nat_cptr.p, 1, nat,
+                              ipart.p + cl.blong.iptr_h.back());
+  const std::vector<int32_t> nptr = {0, a.n};
+  double* nrm = c.dscal + 112;
+  auto residual_norm = [&] {
+    const int64_t T = phase_tasks_h(nptr, nat, 0, G);
+    if (G == 8) count_launch(), relax_task_kernel<8, false><<<(unsigned)T, kRT, 0, c.s>>>(no, 0, b, x, r);
+    else count_launch(), relax_task_kernel<1, false><<<(unsigned)T, kRT, 0, c.s>>>(no, 0, b, x, r);
+    if (no.nsrows) count_launch(), relax_resfin_kernel<<<blocks_for(no.nsrows), kThreads, 0, c.s>>>(no, b, x, r);
+    tree_norm2(c, r, a.n, nrm);
+    CK_LAUNCH();
+  };
+  auto sweep = [&] {
+    for (int32_t cc = 0; cc < cl.ncolors; ++cc) {
+      const int64_t T = phase_tasks_h(cl.cptr_h, cl.blong, cc, G);
+      if (T == 0) continue;
+      if (G == 8) count_launch(), relax_task_kernel<8, true><<<(unsigned)T, kRT, 0, c.s>>>(po, cc, b, x, r);
+      else count_launch(), relax_task_kernel<1, true><<<(unsigned)T, kRT, 0, c.s>>>(po, cc, b, x, r);
+    }
+    subtract_mean_tree(c, x, a.n);
+    residual_norm();
+  };
+  residual_norm();
+  const double r0 = read_scalar(c, nrm);  // tree_norm2 returns the norm
+  if (getenv("LAMG_RELAX_TRACE")) {
+    residual_exact(c, a, b, x, r, nullptr, 0);
+    tree_norm2(c, r, a.n, nrm);
+    const double rx = read_scalar(c, nrm);
+    tree_norm2(c, b, a.n, nrm);
+    const double nb = read_scalar(c, nrm);
+    tree_norm2(c, x, a.n, nrm);
+    const double nx = read_scalar(c, nrm);
+    fprintf(stderr, "[relax] r0 tasks %.6e exact %.6e |b| %.6e |x| %.6e n %d\n", r0, rx, nb, nx, a.n);
+  }
+  if (r0 == 0.0) return 0;
+  DColor::SweepGraph& g = cl.sweep_graph;
+  if (!g.exec || g.b != b || g.x != x || g.r != r) {
+    if (g.exec) CK(cudaGraphExecDestroy(g.exec));
+    g.exec = nullptr;
+    const long long l0 = t_launches;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+    sweep();
+    CK(cudaStreamEndCapture(c.s, &graph));
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    g.launches = t_launches - l0;
+    g_launches -= g.launches;  // counted when the graph runs
+    t_launches = l0;
+    g.b = b, g.x = x, g.r = r;
+  }
+  const double target = 1e-12 * r0;
+  int sweeps = 0;
+  static const bool nograph = getenv("LAMG_RELAX_NOGRAPH") != nullptr;
+  for (; sweeps < 400;) {
+    if (nograph) {
+      sweep();
+    } else {
+      CK(cudaGraphLaunch(g.exec, c.s));
+      t_launches += g.launches;
+      g_launches += g.launches;
+    }
+    ++sweeps;
+    const double rn = read_scalar(c, nrm);
+    if (getenv("LAMG_RELAX_TRACE")) fprintf(stderr, "[relax] sweep %d |r| %.6e (r0 %.6e)\n", sweeps, rn, r0);
+    if (rn <= target) break;
+  }
+  return sweeps;
 }
 
 int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
@@ -702,9 +809,17 @@ int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& 
   DVec<uint64_t> ts;
   uint64_t* tsp = nullptr;
   if (timing) {
-    ts.alloc(cl.ncolors + 3, c.s);
+    ts.alloc(cl.ncolors + 3 + 65, c.s);
     ts.zero();
     tsp = ts.p;
+  }
+  if (getenv("LAMG_RELAX_TRACE")) {
+    residual_exact(c, a, b, x, r, nullptr, 0);
+    double* nrm = c.dscal + 112;
+    tree_norm2(c, r, a.n, nrm);
+    const double rx = read_scalar(c, nrm);
+    fprintf(stderr, "[relax coop] exact r0 %.6e blocks %d G %d ncolors %d n %d nsrows %d\n", rx, blocks,
+            cl.group, cl.ncolors, a.n, no.nsrows);
   }
   void* args[] = {&po, &no, &n, (void*)&b, &x, &r, &pp, &sw, &tsp};
   coop_launch(c, k, blocks, threads, args);
@@ -721,6 +836,9 @@ int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& 
     fprintf(stderr, "[relax timing] blocks %d colours %d: GS phases total %.1f us (min %.2f med %.2f max %.2f), "
             "mean+residual %.1f us; items %d long rows %d\n", blocks, nc, tot, sd[0], sd[nc / 2], sd[nc - 1],
             (double)(t[nc + 1] - t[nc - 1]) * 1e-3, cl.blong.iptr_h.back(), cl.blong.ptr_h.back());
+    fprintf(stderr, "[relax] r0 %.6e\n", reinterpret_cast<const double*>(t.data())[nc + 3 + 64]);
+    for (int i = 0; i < std::min(sweeps, 64); ++i)
+      fprintf(stderr, "[relax] sweep %d |r| %.6e\n", i + 1, reinterpret_cast<const double*>(t.data())[nc + 3 + i]);
     for (int i = 0; i < nc; i += std::max(1, nc / 16))
       fprintf(stderr, "  colour %d: %.2f us rows %d items %d long %d\n", i, d[i], cl.cptr_h[i + 1] - cl.cptr_h[i],
               cl.blong.iptr_h[i + 1] - cl.blong.iptr_h[i], cl.blong.ptr_h[i + 1] - cl.blong.ptr_h[i]);
@@ -779,24 +897,31 @@ void prepare_throughput(Ctx& c, DHier& h) {
     DLevel& L = *h.levels[l];
     const bool smooths = (L.coarsest == CM_RELAX) ||
                          (L.coarsest == CM_NONE && l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_AGG);
-    if (smooths && !L.color) {
-      auto col = std::make_unique<DColor>();
-      build_coloring(c, L.op.view(), L.sched, *col);
-      // append the colour pointers after rp for the single-CTA kernel
-      DVec<int64_t> rp2(L.op.n + 1 + (col->ncolors + 2) / 2 + 1, c.s);
-      CK(cudaMemcpyAsync(rp2.p, col->rp.p, sizeof(int64_t) * (L.op.n + 1), cudaMemcpyDeviceToDevice, c.s));
-      CK(cudaMemcpyAsync(rp2.p + L.op.n + 1, col->cptr_h.data(), sizeof(int32_t) * (col->ncolors + 1),
-                         cudaMemcpyHostToDevice, c.s));
-      col->rp = std::move(rp2);
-      L.color = std::move(col);
-    }
+    if (smooths && !L.color) L.color = make_color(c, L.op.view(), L.sched);
     if (L.direct) build_direct_inverse(c, *L.direct);
-    std::vector<int64_t> nrp((size_t)L.op.n + 1);
-    L.op.rp.download(nrp.data(), L.op.n + 1);
-    c.sync();
-    build_long_rows(c, nrp, std::vector<int32_t>{0, L.op.n}, L.blong_nat);
+    build_natural_long_rows(c, L.op.view(), L.blong_nat);
   }
   c.sync();
+}
+
+std::unique_ptr<DColor> make_color(Ctx& c, const CSRv& a, const Schedule& sch) {
+  auto col = std::make_unique<DColor>();
+  build_coloring(c, a, sch, *col);
+  // append the colour pointers after rp for the single-CTA kernel
+  DVec<int64_t> rp2(a.n + 1 + (col->ncolors + 2) / 2 + 1, c.s);
+  CK(cudaMemcpyAsync(rp2.p, col->rp.p, sizeof(int64_t) * (a.n + 1), cudaMemcpyDeviceToDevice, c.s));
+  CK(cudaMemcpyAsync(rp2.p + a.n + 1, col->cptr_h.data(), sizeof(int32_t) * (col->ncolors + 1),
+                     cudaMemcpyHostToDevice, c.s));
+  col->rp = std::move(rp2);
+  c.sync();
+  return col;
+}
+
+void build_natural_long_rows(Ctx& c, const CSRv& a, LongRows& out) {
+  std::vector<int64_t> nrp((size_t)a.n + 1);
+  CK(cudaMemcpyAsync(nrp.data(), a.rp, sizeof(int64_t) * (a.n + 1), cudaMemcpyDeviceToHost, c.s));
+  c.sync();
+  build_long_rows(c, nrp, std::vector<int32_t>{0, a.n}, out);
 }
 
 }  // namespace lamgb

@@ -126,3 +126,35 @@ def test_throughput_coarsest_inverse(n, ctx):
         want = port.coarsest_direct(a, b)
         assert np.all(np.isfinite(x))
         assert np.linalg.norm(x - want) <= 1e-10 * np.linalg.norm(want)
+
+
+RELAX_GRAPHS = {
+    "rmat_12": lambda: G.rmat(12, seed=5),
+    "chunglu_8k": lambda: G.chung_lu(1 << 13, seed=4),
+    "rmat_14": lambda: G.rmat(14, seed=7),
+    "rmat_17": lambda: G.rmat(17, seed=8),
+}
+
+
+@pytest.mark.parametrize("path", ["coop", "graph"])
+@pytest.mark.parametrize("name", list(RELAX_GRAPHS))
+def test_throughput_relaxation_coarsest(name, path, ctx, monkeypatch):
+    """RelaxationSolver (coarse_solver.cpp:82-93) in THROUGHPUT mode, both the
+    one-launch cooperative form and the per-sweep graph form: the iteration
+    reaches the reference's stopping test (|r| <= 1e-12 |r0|) and lands on the
+    reference's solution (different sweep order: within 1e-7 relative)."""
+    from oracle import Oracle
+    from paper_1108_1310_b200.lamg import Kernels
+    monkeypatch.setenv("LAMG_RELAX_PATH", path)
+    a = RELAX_GRAPHS[name]()
+    b = G.random_vector(a.n, 3, True)
+    x0 = G.random_vector(a.n, 4)
+    gpu = Kernels(ctx)
+    x = gpu.coarsest_relax(a, b, x0)
+    r0 = np.linalg.norm(gpu.residual(a, b, x0))
+    r = np.linalg.norm(gpu.residual(a, b, x))
+    assert np.all(np.isfinite(x))
+    assert r <= 2e-12 * r0, (r, r0)
+    want = Oracle("port").coarsest_relax(a, b, x0)
+    dx, dw = x - x.mean(), want - want.mean()
+    assert np.linalg.norm(dx - dw) <= 1e-7 * np.linalg.norm(dw)
