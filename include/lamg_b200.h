@@ -202,6 +202,35 @@ int lamg_hier_download_colors(const lamg_hier *h, int32_t level, int32_t *row_id
 int lamg_hier_smooth(lamg_ctx *ctx, const lamg_hier *h, int32_t level, int32_t nrhs, const double *b,
                      double *x, int32_t sweeps);
 
+/* ---- fine-level node-block partition with halo exchange (SURVEY 8(e)
+ * mode 2). A level operator split into `nparts` contiguous row blocks
+ * (bounds[nparts+1], balanced by rows + entries); block p is a local CSR over
+ * [owned rows | ghost columns]. A coloured sweep exchanges ghosts after every
+ * colour (NCCL send/recv between ranks, or -- comm == NULL -- every part
+ * owned by this process on its device). Results are bit-identical to the
+ * single-device THROUGHPUT smoother and residual. ---------------------- */
+typedef struct lamg_comm lamg_comm;
+typedef struct lamg_part_level lamg_part_level;
+int lamg_comm_unique_id(char id[128]);                           /* ncclGetUniqueId */
+int lamg_comm_create(lamg_ctx *ctx, int32_t nranks, int32_t rank, const char id[128], lamg_comm **out);
+void lamg_comm_destroy(lamg_comm *comm);
+/* host-only (no GPU): the partition plan */
+int lamg_part_bounds(int32_t n, const int64_t *row_ptr, int32_t nparts, int32_t *bounds);
+int lamg_part_plan_sizes(const lamg_csr *a, const int32_t *bounds, int32_t nparts, int32_t part, int32_t *nloc,
+                         int32_t *nghost, int64_t *nnz, int32_t *nsend);
+int lamg_part_plan(const lamg_csr *a, const int32_t *bounds, int32_t nparts, int32_t part, int64_t *row_ptr,
+                   int32_t *col, int32_t *ghost_gid, int32_t *recv_ptr, int32_t *send_ptr, int32_t *send_idx);
+/* device: a (host CSR, the whole level) is partitioned by bounds; this
+ * process owns parts [first_part, first_part + nown) */
+int lamg_part_level_create(lamg_ctx *ctx, const lamg_csr *a, const int32_t *bounds, int32_t nparts,
+                           int32_t first_part, int32_t nown, lamg_comm *comm, lamg_part_level **out);
+void lamg_part_level_destroy(lamg_part_level *pl);
+/* global host vectors [n]: owned rows are read (b, x) and written (x, r) */
+int lamg_part_smooth(lamg_part_level *pl, const double *b, double *x, int32_t sweeps);
+int lamg_part_residual(lamg_part_level *pl, const double *b, const double *x, double *r);
+/* device-resident timing of `sweeps` partitioned sweeps (+ one residual) */
+int lamg_part_time(lamg_part_level *pl, int32_t sweeps, float *ms);
+
 /* ---- kernel timing (bench roofline): CUDA events around the finest-level
  * residual and Gauss-Seidel launches of the solves issued on ctx ---------- */
 int lamg_ctx_profile(lamg_ctx *ctx, int enable);

@@ -65,6 +65,8 @@ def lib():
         L.lamg_ctx_destroy.restype = None
         L.lamg_hier_destroy.restype = None
         L.lamg_graph_destroy.restype = None
+        L.lamg_comm_destroy.restype = None
+        L.lamg_part_level_destroy.restype = None
         _lib = L
     return _lib
 

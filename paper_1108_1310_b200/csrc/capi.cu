@@ -8,6 +8,7 @@
 #include <string>
 
 #include "batch.cuh"
+#include "part.cuh"
 #include "solve.cuh"
 
 using namespace lamgb;
@@ -291,6 +292,8 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   c.rpart.release();
   c.ripart.release();
   c.rcptr.release();
+  c.rtpart.release();
+  c.rtcptr.release();
   c.res_csr = DCSR();
   c.res_stage.f_diag.release();
   c.res_stage.f_ptr.release();
@@ -1017,5 +1020,154 @@ int lamg_credit_takes(double gamma, int32_t count, int32_t* out) {
 double lamg_flat_mu(double q) { return 2.0 * q / (q + 1.0); }
 
 uint64_t lamg_rng_derive(uint64_t seed, uint64_t stream) { return rng_derive_host(seed, stream); }
+
+// ------------------------------------------------- fine-level partition
+struct lamg_comm {
+  std::unique_ptr<Comm> c;
+};
+struct lamg_part_level {
+  lamg_ctx* ctx;
+  std::unique_ptr<PartLevel> pl;
+  int32_t n;
+};
+
+int lamg_comm_unique_id(char id[128]) {
+  return guarded([&] { comm_unique_id(id); });
+}
+
+int lamg_comm_create(lamg_ctx* ctx, int32_t nranks, int32_t rank, const char id[128], lamg_comm** out) {
+  *out = nullptr;
+  return guarded([&] {
+    set_device(ctx->c);
+    auto* cm = new lamg_comm();
+    try {
+      cm->c = std::make_unique<Comm>(nranks, rank, id);
+    } catch (...) {
+      delete cm;
+      throw;
+    }
+    *out = cm;
+  });
+}
+
+void lamg_comm_destroy(lamg_comm* comm) { delete comm; }
+
+static std::vector<int32_t> bounds_of(const int32_t* bounds, int32_t nparts, int32_t n) {
+  if (nparts < 1) throw LamgError(LAMG_E_ARGUMENT, "partition needs at least one part");
+  std::vector<int32_t> b(bounds, bounds + nparts + 1);
+  if (b[0] != 0 || b[nparts] != n) throw LamgError(LAMG_E_ARGUMENT, "bounds must run from 0 to n");
+  for (int32_t p = 0; p < nparts; ++p)
+    if (b[p + 1] < b[p]) throw LamgError(LAMG_E_ARGUMENT, "bounds must be ascending");
+  return b;
+}
+
+int lamg_part_bounds(int32_t n, const int64_t* row_ptr, int32_t nparts, int32_t* bounds) {
+  return guarded([&] {
+    std::vector<int32_t> b;
+    part_bounds(n, row_ptr, nparts, b);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+int lamg_part_plan_sizes(const lamg_csr* a, const int32_t* bounds, int32_t nparts, int32_t part, int32_t* nloc,
+                         int32_t* nghost, int64_t* nnz, int32_t* nsend) {
+  return guarded([&] {
+    const PartPlan pl = build_part_plan(a->n, a->row_ptr, a->col, a->val, a->diag, bounds_of(bounds, nparts, a->n),
+                                        part);
+    *nloc = pl.nloc;
+    *nghost = pl.nghost;
+    *nnz = (int64_t)pl.col.size();
+    *nsend = (int32_t)pl.send_idx.size();
+  });
+}
+
+int lamg_part_plan(const lamg_csr* a, const int32_t* bounds, int32_t nparts, int32_t part, int64_t* row_ptr,
+                   int32_t* col, int32_t* ghost_gid, int32_t* recv_ptr, int32_t* send_ptr, int32_t* send_idx) {
+  return guarded([&] {
+    const PartPlan pl = build_part_plan(a->n, a->row_ptr, a->col, a->val, a->diag, bounds_of(bounds, nparts, a->n),
+                                        part);
+    std::copy(pl.rp.begin(), pl.rp.end(), row_ptr);
+    std::copy(pl.col.begin(), pl.col.end(), col);
+    std::copy(pl.ghost_gid.begin(), pl.ghost_gid.end(), ghost_gid);
+    std::copy(pl.recv_ptr.begin(), pl.recv_ptr.end(), recv_ptr);
+    std::copy(pl.send_ptr.begin(), pl.send_ptr.end(), send_ptr);
+    std::copy(pl.send_idx.begin(), pl.send_idx.end(), send_idx);
+  });
+}
+
+int lamg_part_level_create(lamg_ctx* ctx, const lamg_csr* a, const int32_t* bounds, int32_t nparts,
+                           int32_t first_part, int32_t nown, lamg_comm* comm, lamg_part_level** out) {
+  *out = nullptr;
+  return guarded([&] {
+    WITH_CSR(ctx, a);
+    const std::vector<int32_t> b = bounds_of(bounds, nparts, a->n);
+    std::vector<int64_t> rp(a->row_ptr, a->row_ptr + a->n + 1);
+    std::vector<int32_t> col(a->col, a->col + 2 * a->m);
+    std::vector<double> val(a->val, a->val + 2 * a->m), diag(a->diag, a->diag + a->n);
+    auto* h = new lamg_part_level();
+    h->ctx = ctx;
+    h->n = a->n;
+    try {
+      h->pl = std::make_unique<PartLevel>(c, av, rp, col, val, diag, b, first_part, nown, comm ? comm->c.get() : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void lamg_part_level_destroy(lamg_part_level* pl) {
+  if (!pl) return;
+  cudaStreamSynchronize(pl->ctx->c.s);
+  delete pl;
+}
+
+int lamg_part_smooth(lamg_part_level* h, const double* b, double* x, int32_t sweeps) {
+  return guarded([&] {
+    Ctx& c = h->ctx->c;
+    set_device(c);
+    auto db = up(c, b, h->n);
+    auto dx = up(c, x, h->n);
+    h->pl->load(db.p, dx.p);
+    h->pl->sweep(sweeps);
+    h->pl->store(dx.p, nullptr);
+    dx.download(x, h->n);
+    c.sync();
+  });
+}
+
+int lamg_part_residual(lamg_part_level* h, const double* b, const double* x, double* r) {
+  return guarded([&] {
+    Ctx& c = h->ctx->c;
+    set_device(c);
+    auto db = up(c, b, h->n);
+    auto dx = up(c, x, h->n);
+    auto dr = up(c, r, h->n);
+    h->pl->load(db.p, dx.p);
+    h->pl->residual();
+    h->pl->store(nullptr, dr.p);
+    dr.download(r, h->n);
+    c.sync();
+  });
+}
+
+int lamg_part_time(lamg_part_level* h, int32_t sweeps, float* ms) {
+  return guarded([&] {
+    Ctx& c = h->ctx->c;
+    set_device(c);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, c.s));
+    h->pl->sweep(sweeps);
+    h->pl->residual();
+    CK(cudaEventRecord(e1, c.s));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
 
 }  // extern "C"

@@ -211,6 +211,9 @@ struct Ctx {
   DVec<double> bscratch;        // batched long-row chunk sums (grown on demand)
   DVec<double> rpart, ripart;   // cooperative relaxation: block partials, chunk partials
   DVec<int32_t> rcptr;          // cooperative relaxation: natural-order range {0, n}
+  DVec<double> rtpart;          // residual_tasks: chunk partials
+  DVec<int32_t> rtcptr;         // residual_tasks: {0, n} of the last operator
+  int32_t rtcptr_n = -1;
   // per-kernel API results kept until taken
   DCSR res_csr;
   struct {

@@ -208,6 +208,7 @@ void relax_solve(Ctx& c, const CSRv& a, const Schedule& sch, const DColor* col, 
 // throughput mode (throughput.cu)
 void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out);
 void gs_colored(Ctx& c, const DColor& col, int32_t n, const double* b, double* x, int sweeps);
+void gs_colored_one(Ctx& c, const DColor& col, const double* b, double* x, int32_t colour);
 // throughput residual r = b - A x with `group` lanes per row (tree-folded rows)
 void residual_tp(Ctx& c, const CSRv& a, const double* b, const double* x, double* r, const DColor& cl);
 inline int row_group_for(int64_t n, int64_t m) {
@@ -218,6 +219,12 @@ void build_direct_inverse(Ctx& c, DDirect& d);
 // whole relaxation-coarsest solve in one cooperative launch; returns sweeps
 int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
                        double* r);
+// THROUGHPUT residual for operators with long rows (hubs chunked over CTAs)
+// group: lanes per short row (1 or 8; <= 0: residual_tasks_group(a, nat))
+void residual_tasks(Ctx& c, const CSRv& a, const LongRows& nat, const double* b, const double* x, double* r,
+                    int group = 0);
+int residual_tasks_group(const CSRv& a, const LongRows& nat);
+inline bool has_long_rows(const LongRows& L) { return !L.ptr_h.empty() && (L.ptr_h.back() > 0 || L.iptr_h.back() > 0); }
 // the same as a per-sweep CUDA graph of task launches (large levels)
 int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
                         double* r);

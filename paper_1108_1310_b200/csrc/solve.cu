@@ -364,6 +364,7 @@ struct Driver {
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
     if (K > 1) bresidual(c, L.op.view(), L.blong_nat, b, x, r, K);
+    else if (!exact && has_long_rows(L.blong_nat)) residual_tasks(c, L.op.view(), L.blong_nat, b, x, r);
     else if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
     else residual_exact(c, L.op.view(), b, x, r, L.sched.heavy_nat.p, L.sched.nheavy_nat);
     if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K);

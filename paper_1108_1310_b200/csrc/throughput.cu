@@ -351,24 +351,27 @@ void gs_colored(Ctx& c, const DColor& cl, int32_t n, const double* b, double* x,
     return;
   }
   for (int sw = 0; sw < sweeps; ++sw)
-    for (int32_t cc = 0; cc < cl.ncolors; ++cc) {
-      int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
-      if (i1 <= i0) continue;
-      const int64_t rows = i1 - i0;
-      const int32_t nh = cl.hptr_h.empty() ? 0 : cl.hptr_h[cc + 1] - cl.hptr_h[cc];
-      if (nh)
-        count_launch(), gs_heavy_kernel<<<nh, 256, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
-                                                             cl.heavy.p + cl.hptr_h[cc], b, x);
-      if (cl.group == 1)
-        count_launch(), gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
-                                                                             cl.row_ids.p, b, x, i0, i1);
-      else if (cl.group == 4)
-        count_launch(), gs_color_group_kernel<4><<<blocks_for(rows * 4), kThreads, 0, c.s>>>(
-            cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
-      else
-        count_launch(), gs_color_group_kernel<8><<<blocks_for(rows * 8), kThreads, 0, c.s>>>(
-            cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
-    }
+    for (int32_t cc = 0; cc < cl.ncolors; ++cc) gs_colored_one(c, cl, b, x, cc);
+}
+
+// the launches of one colour of a coloured sweep (per-colour form of gs_colored)
+void gs_colored_one(Ctx& c, const DColor& cl, const double* b, double* x, int32_t cc) {
+  const int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
+  if (i1 <= i0) return;
+  const int64_t rows = i1 - i0;
+  const int32_t nh = cl.hptr_h.empty() ? 0 : cl.hptr_h[cc + 1] - cl.hptr_h[cc];
+  if (nh)
+    count_launch(), gs_heavy_kernel<<<nh, 256, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
+                                                         cl.heavy.p + cl.hptr_h[cc], b, x);
+  if (cl.group == 1)
+    count_launch(), gs_color_kernel<<<blocks_for(rows), kThreads, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
+                                                                         cl.row_ids.p, b, x, i0, i1);
+  else if (cl.group == 4)
+    count_launch(), gs_color_group_kernel<4><<<blocks_for(rows * 4), kThreads, 0, c.s>>>(
+        cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
+  else
+    count_launch(), gs_color_group_kernel<8><<<blocks_for(rows * 8), kThreads, 0, c.s>>>(
+        cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, b, x, i0, i1);
   CK_LAUNCH();
 }
 
@@ -693,6 +696,37 @@ static int64_t phase_tasks_h(const std::vector<int32_t>& cptr, const LongRows& L
   const int rpb = kRT / G;
   return (int64_t)(L.iptr_h[c + 1] - L.iptr_h[c]) + (L.ptr_h[c + 1] - L.ptr_h[c] + 7) / 8 +
          ((int64_t)(cptr[c + 1] - cptr[c]) + rpb - 1) / rpb;
+}
+
+// THROUGHPUT residual r = b - A x of an operator with long rows (power-law
+// levels): the relaxation's residual tasks (chunked hubs, warp long rows,
+// short-row blocks), super-long rows finished from their chunk partials.
+int residual_tasks_group(const CSRv& a, const LongRows& nat) {
+  return row_group_for(a.n, a.m) == 8 || nat.ptr_h.back() > 0 ? 8 : 1;
+}
+
+void residual_tasks(Ctx& c, const CSRv& a, const LongRows& nat, const double* b, const double* x, double* r,
+                    int group) {
+  if (a.n == 0) return;
+  const int G = group > 0 ? group : residual_tasks_group(a, nat);
+  DVec<double>& ipart = c.rtpart;
+  const int64_t nitems = std::max<int64_t>(1, (int64_t)nat.iptr_h.back());
+  if (ipart.n < nitems) ipart.alloc(nitems, c.s);
+  DVec<int32_t>& cp = c.rtcptr;
+  if (cp.n < 2 || cp.s != c.s) cp.alloc(2, c.s);
+  if (c.rtcptr_n != a.n) {
+    const int32_t ncp[2] = {0, a.n};
+    cp.upload(ncp, 2);
+    c.rtcptr_n = a.n;
+  }
+  const RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, cp.p, 1, nat, ipart.p);
+  const std::vector<int32_t> nptr = {0, a.n};
+  const int64_t T = phase_tasks_h(nptr, nat, 0, G);
+  double* xm = const_cast<double*>(x);
+  if (G == 8) count_launch(), relax_task_kernel<8, false><<<(unsigned)T, kRT, 0, c.s>>>(no, 0, b, xm, r);
+  else count_launch(), relax_task_kernel<1, false><<<(unsigned)T, kRT, 0, c.s>>>(no, 0, b, xm, r);
+  if (no.nsrows) count_launch(), relax_resfin_kernel<<<blocks_for(no.nsrows), kThreads, 0, c.s>>>(no, b, x, r);
+  CK_LAUNCH();
 }
 
 // RelaxationSolver::solve (coarse_solver.cpp:82-93), THROUGHPUT, for large

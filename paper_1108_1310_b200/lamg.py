@@ -694,3 +694,99 @@ class Kernels:
 
     def setup(self, a, gamma=1.5, seed=1, coarsest_n=150, tv_sweeps=3, tv_count_finest=4, tv_count_max=10):
         return setup(a, SetupOptions(gamma, seed, coarsest_n, tv_sweeps, tv_count_finest, tv_count_max), ctx=self.ctx)
+
+
+# ------------------------------------------------ fine-level partition (8(e) mode 2)
+def part_bounds(a, nparts: int) -> np.ndarray:
+    """Contiguous row blocks balanced by rows + entries (host only)."""
+    rp = _i64(a.row_ptr)
+    out = np.empty(nparts + 1, np.int32)
+    _check(_lib.lib().lamg_part_bounds(C.c_int32(a.n), _p(rp), C.c_int32(nparts), _p(out)))
+    return out
+
+
+def part_plan(a, bounds, part: int) -> dict:
+    """Local CSR, ghosts and send/recv lists of one part (host only)."""
+    arg, bounds = _CSRArg(a), _i32(bounds)
+    P = len(bounds) - 1
+    nloc, ngh, nsend, nnz = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+    lib = _lib.lib()
+    _check(lib.lamg_part_plan_sizes(arg.ref(), _p(bounds), C.c_int32(P), C.c_int32(part), C.byref(nloc),
+                                    C.byref(ngh), C.byref(nnz), C.byref(nsend)))
+    d = dict(row_ptr=np.empty(nloc.value + 1, np.int64), col=np.empty(nnz.value, np.int32),
+             ghost_gid=np.empty(ngh.value, np.int32), recv_ptr=np.empty(P + 1, np.int32),
+             send_ptr=np.empty(P + 1, np.int32), send_idx=np.empty(nsend.value, np.int32))
+    _check(lib.lamg_part_plan(arg.ref(), _p(bounds), C.c_int32(P), C.c_int32(part),
+                              *[_p(d[k]) for k in ("row_ptr", "col", "ghost_gid", "recv_ptr", "send_ptr",
+                                                   "send_idx")]))
+    d["lo"], d["hi"] = int(bounds[part]), int(bounds[part + 1])
+    return d
+
+
+class Comm:
+    """NCCL communicator for the partitioned level (one rank per GPU)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.lib().lamg_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.nranks, self.rank = nranks, rank
+        self.p = C.c_void_p()
+        _check(self.ctx.lib.lamg_comm_create(self.ctx.p, C.c_int32(nranks), C.c_int32(rank),
+                                             C.create_string_buffer(uid, 128), C.byref(self.p)))
+
+    def close(self):
+        if self.p and self.p.value:
+            self.ctx.lib.lamg_comm_destroy(self.p)
+            self.p = C.c_void_p()
+
+
+class PartLevel:
+    """A level operator split into row blocks with halo exchange.
+
+    Without `comm` this process owns every part (one device); with an NCCL
+    `comm` it owns part `comm rank` of `nparts`.
+    """
+
+    def __init__(self, a, nparts: int, ctx: Context | None = None, bounds=None, comm: Comm | None = None):
+        self.ctx = ctx or default_context()
+        self.n = a.n
+        self.bounds = _i32(bounds if bounds is not None else part_bounds(a, nparts))
+        arg = _CSRArg(a)
+        self.p = C.c_void_p()
+        first, nown = (0, nparts) if comm is None else (comm.rank, 1)
+        _check(self.ctx.lib.lamg_part_level_create(self.ctx.p, arg.ref(), _p(self.bounds), C.c_int32(nparts),
+                                                   C.c_int32(first), C.c_int32(nown),
+                                                   comm.p if comm is not None else None, C.byref(self.p)))
+
+    def smooth(self, b, x, sweeps: int = 1):
+        b, x = _f64(b), _f64(x).copy()
+        _check(self.ctx.lib.lamg_part_smooth(self.p, _p(b), _p(x), C.c_int32(sweeps)))
+        return x
+
+    def residual(self, b, x):
+        b, x = _f64(b), _f64(x)
+        r = np.zeros(self.n)
+        _check(self.ctx.lib.lamg_part_residual(self.p, _p(b), _p(x), _p(r)))
+        return r
+
+    def time(self, sweeps: int) -> float:
+        ms = C.c_float()
+        _check(self.ctx.lib.lamg_part_time(self.p, C.c_int32(sweeps), C.byref(ms)))
+        return ms.value
+
+    def close(self):
+        if getattr(self, "p", None) and self.p.value:
+            self.ctx.lib.lamg_part_level_destroy(self.p)
+            self.p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+

@@ -1,0 +1,176 @@
+"""Fine-level node-block partition with halo exchange (SURVEY.md 8(e) mode 2).
+
+CPU (no GPU): the host partition plan of liblamg_b200.so -- bounds cover
+[0, n) in balanced contiguous blocks, the local CSR maps back to the global
+rows entry for entry, every part's send list to q is exactly q's ghosts from
+it (same order), and a residual computed block by block from owned values
+plus exchanged ghosts equals the global residual. The exchange runs once in
+process and once between two gloo ranks (the N>1 path of the NCCL transport).
+
+GPU: the partitioned coloured sweep and residual (in-process transport, all
+parts on one device) are bit-identical to the single-part ones for 1-4 parts,
+and the single-part sweep is the sequential coloured sweep of the restatement.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_1108_1310_b200 import graphs as G
+
+GRAPHS = {
+    "grid5_24": lambda: G.grid_5pt(24),
+    "grid3d_12": lambda: G.grid3d_7pt(12),
+    "rgg_4k": lambda: G.rgg(1 << 12, seed=3),
+    "rmat_11": lambda: G.rmat(11, seed=5),
+}
+
+
+def _residual(a, b, x):
+    A = sp.csr_matrix((a.val, a.col, a.row_ptr), shape=(a.n, a.n))
+    return b - (a.diag * x + A @ x)
+
+
+def _local_residual(a, d, b, xfull_owned, ghosts):
+    lo, hi = d["lo"], d["hi"]
+    nloc = hi - lo
+    xl = np.concatenate([xfull_owned, ghosts])
+    val = a.val[a.row_ptr[lo]:a.row_ptr[hi]]
+    A = sp.csr_matrix((val, d["col"], d["row_ptr"]), shape=(nloc, nloc + len(d["ghost_gid"])))
+    return b[lo:hi] - (a.diag[lo:hi] * xl[:nloc] + A @ xl)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+@pytest.mark.parametrize("name", list(GRAPHS))
+def test_plan_invariants_and_exchange(name, P):
+    from paper_1108_1310_b200 import lamg as L
+    a = GRAPHS[name]()
+    bounds = L.part_bounds(a, P)
+    assert bounds[0] == 0 and bounds[-1] == a.n and np.all(np.diff(bounds) >= 0)
+    cost = np.diff(a.row_ptr) + 1
+    per = [cost[bounds[p]:bounds[p + 1]].sum() for p in range(P)]
+    assert max(per) <= cost.sum() / P + cost.max() + 1
+    plans = [L.part_plan(a, bounds, p) for p in range(P)]
+    for p, d in enumerate(plans):
+        lo, hi = d["lo"], d["hi"]
+        nloc = hi - lo
+        gid = np.concatenate([np.arange(lo, hi), d["ghost_gid"]]).astype(np.int64)
+        assert np.array_equal(gid[d["col"]], a.col[a.row_ptr[lo]:a.row_ptr[hi]])
+        assert np.array_equal(d["row_ptr"], a.row_ptr[lo:hi + 1] - a.row_ptr[lo])
+        assert np.all(np.diff(d["ghost_gid"]) > 0)
+        assert not np.any((d["ghost_gid"] >= lo) & (d["ghost_gid"] < hi))
+        for q in range(P):
+            ghosts_from_q = d["ghost_gid"][d["recv_ptr"][q]:d["recv_ptr"][q + 1]]
+            assert np.all((ghosts_from_q >= bounds[q]) & (ghosts_from_q < bounds[q + 1]))
+            e = plans[q]
+            sent = e["send_idx"][e["send_ptr"][p]:e["send_ptr"][p + 1]] + e["lo"]
+            assert np.array_equal(sent, ghosts_from_q), (p, q)
+        assert d["send_ptr"][p + 1] == d["send_ptr"][p] and d["recv_ptr"][p + 1] == d["recv_ptr"][p]
+    rng = np.random.default_rng(5)
+    b, x = rng.standard_normal(a.n), rng.standard_normal(a.n)
+    want = _residual(a, b, x)
+    got = np.empty(a.n)
+    for p, d in enumerate(plans):
+        ghosts = np.empty(len(d["ghost_gid"]))
+        for q in range(P):  # exchange: q's send list lands in p's ghost range
+            e = plans[q]
+            ghosts[d["recv_ptr"][q]:d["recv_ptr"][q + 1]] = x[e["lo"] + e["send_idx"][e["send_ptr"][p]:e["send_ptr"][p + 1]]]
+        got[d["lo"]:d["hi"]] = _local_residual(a, d, b, x[d["lo"]:d["hi"]], ghosts)
+    assert np.allclose(got, want, rtol=1e-13, atol=1e-13 * np.abs(want).max())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from paper_1108_1310_b200 import graphs as G2
+    from paper_1108_1310_b200 import lamg as L
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = G2.rmat(10, seed=5)
+    bounds = L.part_bounds(a, world)
+    d = L.part_plan(a, bounds, rank)
+    rng = np.random.default_rng(9)
+    b, x = rng.standard_normal(a.n), rng.standard_normal(a.n)
+    own = x[d["lo"]:d["hi"]]  # a rank knows only its own rows
+    ghosts = torch.zeros(len(d["ghost_gid"]), dtype=torch.float64)
+    ops = []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        s0, s1 = d["send_ptr"][peer], d["send_ptr"][peer + 1]
+        r0, r1 = d["recv_ptr"][peer], d["recv_ptr"][peer + 1]
+        if s1 > s0:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(own[d["send_idx"][s0:s1]].copy()), peer))
+        if r1 > r0:
+            buf = torch.zeros(r1 - r0, dtype=torch.float64)
+            ops.append((dist.P2POp(dist.irecv, buf, peer), r0, r1, buf))
+    reqs = dist.batch_isend_irecv([o if isinstance(o, dist.P2POp) else o[0] for o in ops])
+    for r in reqs:
+        r.wait()
+    for o in ops:
+        if not isinstance(o, dist.P2POp):
+            ghosts[o[1]:o[2]] = o[3]
+    r_loc = _local_residual(a, d, b, own, ghosts.numpy())
+    full = [torch.zeros(1) for _ in range(world)]
+    parts = [None] * world
+    dist.all_gather_object(parts, (d["lo"], r_loc))
+    del full
+    if rank == 0:
+        got = np.empty(a.n)
+        for lo, rl in parts:
+            got[lo:lo + len(rl)] = rl
+        want = _residual(a, b, x)
+        q.put(float(np.abs(got - want).max() / np.abs(want).max()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_halo_exchange():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["grid3d_40", "rgg_64k", "rmat_15"])
+def test_partitioned_sweep_bit_identical(name):
+    from paper_1108_1310_b200 import lamg as L
+    a = {"grid3d_40": lambda: G.grid3d_7pt(40), "rgg_64k": lambda: G.rgg(1 << 16, seed=3),
+         "rmat_15": lambda: G.rmat(15, seed=5)}[name]()
+    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(a.n)
+    b -= b.mean()
+    x = rng.standard_normal(a.n)
+    one = L.PartLevel(a, 1, ctx=ctx)
+    want_x = one.smooth(b, x, 2)
+    want_r = one.residual(b, want_x)
+    assert np.allclose(want_r, _residual(a, b, want_x), rtol=1e-12, atol=1e-12 * np.abs(want_r).max())
+    for P in (2, 3, 4):
+        pl = L.PartLevel(a, P, ctx=ctx)
+        got_x = pl.smooth(b, x, 2)
+        assert np.array_equal(got_x, want_x), (P, float(np.abs(got_x - want_x).max()))
+        assert np.array_equal(pl.residual(b, want_x), want_r), P
+        pl.close()
+    one.close()
+    ctx.close()

@@ -17,12 +17,13 @@ from paper_1108_1310_b200 import graphs as G  # noqa: E402
 from paper_1108_1310_b200 import lamg as L  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 22
+chung = "--chunglu" in sys.argv  # config 4 shape (Chung-Lu, beta 2.1) at 2^scale nodes
 prof = "--profile" in sys.argv
 ctx = L.Context(0, L.MODE_THROUGHPUT)
 t = time.time()
-a = L.gen_rmat(scale, seed=5, ctx=ctx)
+a = G.chung_lu(1 << scale, seed=4) if chung else L.gen_rmat(scale, seed=5, ctx=ctx)
 torch.cuda.synchronize()
-print(f"rmat{scale}: n={a.n} m={a.m} gen {time.time() - t:.2f}s", flush=True)
+print(f"{'chunglu' if chung else 'rmat'}{scale}: n={a.n} m={a.m} gen {time.time() - t:.2f}s", flush=True)
 t = time.time()
 h = L.setup(a, ctx=ctx)
 torch.cuda.synchronize()

@@ -11,7 +11,7 @@ from paper_1108_1310_b200 import lamg as L  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 ctx = L.Context(0, L.MODE_THROUGHPUT)
-a = L.gen_rmat(scale, seed=5, ctx=ctx)
+a = G.chung_lu(1 << scale, seed=4) if "--chunglu" in sys.argv else L.gen_rmat(scale, seed=5, ctx=ctx)
 h = L.setup(a, ctx=ctx)
 h.prepare_throughput()
 b, x0 = G.gaussian_rhs(a.n, 500), G.default_x0(a.n)
