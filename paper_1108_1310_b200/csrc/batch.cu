@@ -262,6 +262,7 @@ __global__ void bcoarsen_kernel(StageV s, const double* __restrict__ B, double* 
   const int64_t q = t / K;
   const int k = (int)(t % K);
   if (q >= s.coarse_n) return;
+  if (s.ntlong && s.t_ptr[q + 1] - s.t_ptr[q] > kLongT) return;  // bcoarsen_long_kernel
   double v = B[(int64_t)s.poc[q] * K + k];
   for (int64_t j = s.t_ptr[q]; j < s.t_ptr[q + 1]; ++j) {
     const int64_t p = s.t_p[j];
@@ -269,6 +270,32 @@ __global__ void bcoarsen_kernel(StageV s, const double* __restrict__ B, double* 
     v = v - s.f_val[p] * (B[(int64_t)s.f_nodes[i] * K + k] / s.f_diag[i]);
   }
   Bc[t] = v;
+}
+
+// a coarse node with a long contribution list, K columns: 32 strided slices
+// (fixed, so a column's sum does not depend on K), summed in slice order
+template <int K>
+__global__ void __launch_bounds__(kBT) bcoarsen_long_kernel(StageV s, const double* __restrict__ B,
+                                                            double* __restrict__ Bc) {
+  __shared__ double sh[kSL * 32];
+  const int32_t q = s.tlong[blockIdx.x];
+  const int64_t j0 = s.t_ptr[q], j1 = s.t_ptr[q + 1];
+  for (int pr = threadIdx.x; pr < kSL * K; pr += blockDim.x) {
+    const int sl = pr / K, k = pr % K;
+    double acc = 0.0;
+    for (int64_t j = j0 + sl; j < j1; j += kSL) {
+      const int64_t p = s.t_p[j];
+      const int32_t i = s.f_of_p[p];
+      acc += s.f_val[p] * (B[(int64_t)s.f_nodes[i] * K + k] / s.f_diag[i]);
+    }
+    sh[sl * K + k] = acc;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < K) {
+    double t = 0.0;
+    for (int sl = 0; sl < kSL; ++sl) t += sh[sl * K + threadIdx.x];
+    Bc[(int64_t)q * K + threadIdx.x] = B[(int64_t)s.poc[q] * K + threadIdx.x] - t;
+  }
 }
 
 template <int K>
@@ -476,6 +503,7 @@ void bcoarsen_rhs(Ctx& c, const StageV& s, const double* B, double* Bc, int K) {
   dispatch_k(K, [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
     count_launch(), bcoarsen_kernel<KK><<<bblocks((int64_t)s.coarse_n * KK), kBT, 0, c.s>>>(s, B, Bc);
+    if (s.ntlong) count_launch(), bcoarsen_long_kernel<KK><<<s.ntlong, kBT, 0, c.s>>>(s, B, Bc);
   });
   CK_LAUNCH();
 }

@@ -95,6 +95,7 @@ void upload_stage(Ctx& c, int32_t parent_n, int32_t coarse_n, int32_t nf, const 
   s.cop = up(c, cop, parent_n);
   s.poc = up(c, poc, coarse_n);
   build_stage_transpose(c, coarse_n, nf, s.f_ptr.p, s.f_nbr.p, s.cop.p, s.nnzf, s.t_ptr, s.t_p, s.f_of_p);
+  s.ntlong = stage_long_lists(c, coarse_n, s.t_ptr.p, s.tlong);
 }
 
 int solve_common(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, bool dev,

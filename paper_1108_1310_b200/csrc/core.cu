@@ -491,6 +491,7 @@ void interpolate(Ctx& c, int32_t fine_n, const int32_t* agg, const double* ec, d
 __global__ void coarsen_rhs_kernel(StageV s, const double* __restrict__ b, double* __restrict__ bc) {
   int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= s.coarse_n) return;
+  if (s.ntlong && s.t_ptr[k + 1] - s.t_ptr[k] > kLongT) return;  // coarsen_rhs_long_kernel
   double v = b[s.poc[k]];
   for (int64_t j = s.t_ptr[k]; j < s.t_ptr[k + 1]; ++j) {
     const int64_t p = s.t_p[j];
@@ -500,10 +501,70 @@ __global__ void coarsen_rhs_kernel(StageV s, const double* __restrict__ b, doubl
   }
   bc[k] = v;
 }
+// coarse nodes with long contribution lists (hubs next to many eliminated
+// nodes): one CTA each. The products f_val*(b_f/a_ff) are formed in parallel
+// exactly as the sequential loop rounds them; VALIDATE folds them in (f, p)
+// order with one thread (bit-exact), THROUGHPUT with a fixed block tree.
+__global__ void coarsen_rhs_long_kernel(StageV s, const double* __restrict__ b, double* __restrict__ bc) {
+  __shared__ double sh[kThreads];
+  __shared__ double sh_v;
+  const int32_t k = s.tlong[blockIdx.x];
+  const int64_t j0 = s.t_ptr[k], j1 = s.t_ptr[k + 1];
+  if (s.exact) {
+    if (threadIdx.x == 0) sh_v = b[s.poc[k]];
+    for (int64_t c0 = j0; c0 < j1; c0 += kThreads) {
+      __syncthreads();
+      const int64_t j = c0 + threadIdx.x;
+      if (j < j1) {
+        const int64_t p = s.t_p[j];
+        const int32_t i = s.f_of_p[p];
+        sh[threadIdx.x] = s.f_val[p] * (b[s.f_nodes[i]] / s.f_diag[i]);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int cnt = j1 - c0 < kThreads ? (int)(j1 - c0) : kThreads;
+        double v = sh_v;
+        for (int q = 0; q < cnt; ++q) v = v - sh[q];
+        sh_v = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) bc[k] = sh_v;
+    return;
+  }
+  double acc = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += kThreads) {
+    const int64_t p = s.t_p[j];
+    const int32_t i = s.f_of_p[p];
+    acc += s.f_val[p] * (b[s.f_nodes[i]] / s.f_diag[i]);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bc[k] = b[s.poc[k]] - sh[0];
+}
+
 void coarsen_rhs(Ctx& c, const StageV& s, const double* b, double* bc) {
   if (s.coarse_n == 0) return;
   count_launch(), coarsen_rhs_kernel<<<blocks_for(s.coarse_n), kThreads, 0, c.s>>>(s, b, bc);
+  if (s.ntlong) count_launch(), coarsen_rhs_long_kernel<<<s.ntlong, kThreads, 0, c.s>>>(s, b, bc);
   CK_LAUNCH();
+}
+
+__global__ void long_t_flags_kernel(const int64_t* t_ptr, int32_t n, uint8_t* f) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) f[k] = t_ptr[k + 1] - t_ptr[k] > kLongT;
+}
+int32_t stage_long_lists(Ctx& c, int32_t coarse_n, const int64_t* t_ptr, DVec<int32_t>& out) {
+  out.alloc(std::max(coarse_n, 1), c.s);
+  if (coarse_n == 0) return 0;
+  DVec<uint8_t> f(coarse_n, c.s);
+  count_launch(), long_t_flags_kernel<<<blocks_for(coarse_n), kThreads, 0, c.s>>>(t_ptr, coarse_n, f.p);
+  CK_LAUNCH();
+  return (int32_t)select_flagged_index(c, f.p, out.p, coarse_n);
 }
 
 __global__ void gather_kernel(double* dst, const double* src, const int32_t* idx, int64_t n) {

@@ -87,7 +87,13 @@ struct StageV {
   const int64_t* t_ptr;  // per coarse node: contributions (f asc, p asc)
   const int64_t* t_p;
   const int32_t* f_of_p;
+  const int32_t* tlong = nullptr;  // coarse nodes with more than kLongT contributions (a CTA each)
+  int32_t ntlong = 0;
+  bool exact = true;               // VALIDATE: long lists folded in (f, p) order by one thread
 };
+constexpr int64_t kLongT = 64;
+// coarse nodes of a stage whose contribution lists exceed kLongT entries
+int32_t stage_long_lists(Ctx& c, int32_t coarse_n, const int64_t* t_ptr, DVec<int32_t>& out);
 void coarsen_rhs(Ctx& c, const StageV& s, const double* b, double* bc);
 void inject(Ctx& c, const StageV& s, const double* x, double* xc);
 void backsub(Ctx& c, const StageV& s, const double* xc, const double* b, double* x);

@@ -26,9 +26,11 @@ struct DStage {
   DVec<int32_t> cop, poc;
   DVec<int64_t> t_ptr, t_p;
   DVec<int32_t> f_of_p;
-  StageV view() const {
+  DVec<int32_t> tlong;  // coarse nodes with long contribution lists
+  int32_t ntlong = 0;
+  StageV view(bool exact = true) const {
     return StageV{parent_n, coarse_n, nf, f_nodes.p, f_diag.p, f_ptr.p, f_nbr.p, f_val.p,
-                  cop.p, poc.p, t_ptr.p, t_p.p, f_of_p.p};
+                  cop.p, poc.p, t_ptr.p, t_p.p, f_of_p.p, tlong.p, ntlong, exact};
   }
 };
 

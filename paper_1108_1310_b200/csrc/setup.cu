@@ -458,6 +458,7 @@ void schur_reduce(Ctx& c, const CSRv& a, const int32_t* f, int32_t nf, const int
   fold_contribs_and_assemble(c, nc, total, keys, w, coarse);
   c.work += (double)(a.m + coarse.m);
   build_stage_transpose(c, nc, nf, st.f_ptr.p, st.f_nbr.p, st.cop.p, st.nnzf, st.t_ptr, st.t_p, st.f_of_p);
+  st.ntlong = stage_long_lists(c, nc, st.t_ptr.p, st.tlong);
 }
 
 // elimination.cpp:107-124

@@ -297,7 +297,7 @@ struct Driver {
     for (size_t s = 0; s < S; ++s) {
       double* out = s + 1 < S ? ws.lv[0].stage_rhs[s + 1].p : ws.lv[1].b.p;
       if (K > 1) bcoarsen_rhs(c, st[s]->view(), in, out, K);
-      else coarsen_rhs(c, st[s]->view(), in, out);
+      else coarsen_rhs(c, st[s]->view(exact), in, out);
       c.work += (double)st[s]->nnzf;
       in = out;
     }
@@ -319,7 +319,7 @@ struct Driver {
       double* out = s + 1 < S ? w.stage_rhs[s + 1].p : wc.b.p;
       if (!cached) {
         if (K > 1) bcoarsen_rhs(c, st[s]->view(), rhs[s], out, K);
-        else coarsen_rhs(c, st[s]->view(), rhs[s], out);
+        else coarsen_rhs(c, st[s]->view(exact), rhs[s], out);
         c.work += (double)st[s]->nnzf;
       }
       if (s + 1 < S) rhs[s + 1] = out;
