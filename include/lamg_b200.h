@@ -184,6 +184,12 @@ int lamg_solve_batch_dev(lamg_ctx *ctx, const lamg_hier *h, int32_t nrhs, const 
  * lamg_graph_csr gives device pointers for lamg_setup(..., on_device=1, ...). */
 int lamg_gen_rmat(lamg_ctx *ctx, int32_t scale, int32_t edge_factor, double a, double b, double c,
                   uint64_t seed, int32_t keep_lcc, lamg_graph **out);
+/* BASELINE config 4 (Chung-Lu): cdf[n] = normalised cumulative expected
+ * degrees (host-computed, as graphs.chung_lu); `pairs` endpoint pairs drawn
+ * on the device by inverse CDF, self-loops dropped, duplicates merged to
+ * unit weight, largest component kept */
+int lamg_gen_chung_lu(lamg_ctx *ctx, int32_t n, const double *cdf, int64_t pairs, uint64_t seed,
+                      int32_t keep_lcc, lamg_graph **out);
 int lamg_graph_lcc(lamg_ctx *ctx, const lamg_csr *a, int on_device, lamg_graph **out);
 int lamg_graph_csr(const lamg_graph *g, lamg_csr *out_device_view);
 int lamg_graph_download(const lamg_graph *g, int64_t *row_ptr, int32_t *col, double *val, double *diag);

@@ -228,6 +228,7 @@ int solve_batch_common(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const do
 namespace lamgb {
 void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc, uint64_t seed, bool lcc, DCSR& out);
 bool largest_component_dev(Ctx& c, const CSRv& a, DCSR& out);
+void gen_chung_lu(Ctx& c, int32_t n, const double* cdf_host, int64_t pairs, uint64_t seed, bool lcc, DCSR& out);
 }  // namespace lamgb
 
 struct lamg_graph {
@@ -507,6 +508,25 @@ int lamg_gen_rmat(lamg_ctx* ctx, int32_t scale, int32_t edge_factor, double a, d
     g->device = c.device;
     try {
       gen_rmat(c, scale, edge_factor, a, b, c_, seed, keep_lcc != 0, g->a);
+      c.sync();
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int lamg_gen_chung_lu(lamg_ctx* ctx, int32_t n, const double* cdf, int64_t pairs, uint64_t seed, int32_t keep_lcc,
+                      lamg_graph** out) {
+  *out = nullptr;
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    set_device(c);
+    auto* g = new lamg_graph();
+    g->device = c.device;
+    try {
+      gen_chung_lu(c, n, cdf, pairs, seed, keep_lcc != 0, g->a);
       c.sync();
     } catch (...) {
       delete g;

@@ -46,6 +46,31 @@ __global__ void rmat_kernel(int scale, int64_t S, uint64_t s0, double a, double 
   key[i] = u == v ? ~0ull : (u < v ? (u << scale) | v : (v << scale) | u);
 }
 
+// Chung-Lu (config 4): pair j's endpoints are searchsorted(cdf, U, 'right')
+// of draws j and pairs + j (graphs.chung_lu), clamped to n - 1
+__device__ inline int32_t upper_bound_f64(const double* cdf, int32_t n, double u) {
+  int32_t lo = 0, hi = n;  // first index with cdf[i] > u
+  while (lo < hi) {
+    const int32_t mid = lo + (hi - lo) / 2;
+    if (cdf[mid] <= u) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void chunglu_kernel(const double* __restrict__ cdf, int32_t n, int bits, int64_t pairs, uint64_t s0,
+                               uint64_t* key) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= pairs) return;
+  uint64_t u = (uint64_t)min(upper_bound_f64(cdf, n, unit_at(s0, (uint64_t)j)), n - 1);
+  uint64_t v = (uint64_t)min(upper_bound_f64(cdf, n, unit_at(s0, (uint64_t)(pairs + j))), n - 1);
+  key[j] = u == v ? ~0ull : (u < v ? (u << bits) | v : (v << bits) | u);
+}
+
+__global__ void ones_kernel(double* w, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) w[i] = 1.0;
+}
+
 __global__ void run_heads_kernel(const uint64_t* k, int64_t n, uint8_t* head) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) head[i] = k[i] != ~0ull && (i == 0 || k[i] != k[i - 1]);
@@ -212,18 +237,14 @@ bool largest_component_dev(Ctx& c, const CSRv& a, DCSR& out) {
 
 // R-MAT (BASELINE.json config 5; graphs.py rmat): 2^scale nodes,
 // edge_factor * 2^scale samples, duplicates summed, optional LCC.
-void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc, uint64_t seed, bool lcc,
-              DCSR& out) {
-  if (scale < 1 || scale > 30) throw LamgError(LAMG_E_ARGUMENT, "rmat: scale must be in [1, 30]");
-  const int32_t n = (int32_t)(1u << scale);
-  const int64_t S = (int64_t)edge_factor << scale;
-  const double ab = a + b, abc = a + b + cc;  // graphs.py evaluates a + b + c left to right
-  const uint64_t s0 = seed ? seed : 0x9e3779b97f4a7c15ULL;
+// sampled edge keys (lo << bits | hi, all-ones for self-loops) -> merged
+// edges (weights = multiplicities, or 1 with unit_weights) -> canonical CSR
+// -> largest component
+static void keys_to_graph(Ctx& c, int32_t n, int scale, DVec<uint64_t>& k, int64_t S, bool unit_weights, bool lcc,
+                          DCSR& out) {
   DCSR full;
   {
-    DVec<uint64_t> k(std::max<int64_t>(S, 1), c.s), ks(std::max<int64_t>(S, 1), c.s);
-    count_launch(), rmat_kernel<<<blocks_for(S), kThreads, 0, c.s>>>(scale, S, s0, a, ab, abc, k.p);
-    CK_LAUNCH();
+    DVec<uint64_t> ks(std::max<int64_t>(S, 1), c.s);
     sort_keys_u64(c, k.p, ks.p, S, 64);
     k.release();
     DVec<uint8_t> head(S, c.s);
@@ -250,6 +271,7 @@ void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc,
       count_launch(), runs_to_edges_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ks.p, start.p, E, total, scale, eu.p,
                                                                                ev.p, ew.p);
       CK_LAUNCH();
+      if (unit_weights) count_launch(), ones_kernel<<<blocks_for(E), kThreads, 0, c.s>>>(ew.p, E);
     }
     ks.release();
     start.release();
@@ -264,6 +286,36 @@ void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc,
     }
   }
   out = std::move(full);
+}
+
+void gen_rmat(Ctx& c, int scale, int edge_factor, double a, double b, double cc, uint64_t seed, bool lcc,
+              DCSR& out) {
+  if (scale < 1 || scale > 30) throw LamgError(LAMG_E_ARGUMENT, "rmat: scale must be in [1, 30]");
+  const int32_t n = (int32_t)(1u << scale);
+  const int64_t S = (int64_t)edge_factor << scale;
+  const double ab = a + b, abc = a + b + cc;  // graphs.py evaluates a + b + c left to right
+  const uint64_t s0 = seed ? seed : 0x9e3779b97f4a7c15ULL;
+  DVec<uint64_t> k(std::max<int64_t>(S, 1), c.s);
+  count_launch(), rmat_kernel<<<blocks_for(S), kThreads, 0, c.s>>>(scale, S, s0, a, ab, abc, k.p);
+  CK_LAUNCH();
+  keys_to_graph(c, n, scale, k, S, false, lcc, out);
+}
+
+// BASELINE config 4 (graphs.chung_lu): the normalised cumulative weights
+// come from the host (numpy's pairwise mean and sequential cumsum define
+// them); sampling, merging and the component step run here
+void gen_chung_lu(Ctx& c, int32_t n, const double* cdf_host, int64_t pairs, uint64_t seed, bool lcc, DCSR& out) {
+  if (n < 2) throw LamgError(LAMG_E_ARGUMENT, "chung_lu: n must be at least 2");
+  int bits = 1;
+  while ((1ll << bits) < n) ++bits;
+  const uint64_t s0 = seed ? seed : 0x9e3779b97f4a7c15ULL;
+  DVec<double> cdf(n, c.s);
+  cdf.upload(cdf_host, n);
+  DVec<uint64_t> k(std::max<int64_t>(pairs, 1), c.s);
+  if (pairs) count_launch(), chunglu_kernel<<<blocks_for(pairs), kThreads, 0, c.s>>>(cdf.p, n, bits, pairs, s0, k.p);
+  CK_LAUNCH();
+  cdf.release();
+  keys_to_graph(c, n, bits, k, pairs, true, lcc, out);
 }
 
 }  // namespace lamgb

@@ -405,6 +405,26 @@ def gen_rmat(scale: int, seed: int = 5, edge_factor: int = 16, abcd=(0.57, 0.19,
     return DeviceGraph(ctx, g)
 
 
+def gen_chung_lu(n: int, seed: int = 4, beta: float = 2.1, mean_degree: float = 16.0, lcc: bool = True,
+                 ctx: Context | None = None) -> DeviceGraph:
+    """BASELINE config 4 generator on the device; bit-identical to graphs.chung_lu.
+
+    The expected-degree CDF and the pair count are numpy's (pairwise mean,
+    sequential cumsum), exactly as graphs.chung_lu forms them.
+    """
+    ctx = ctx or default_context()
+    wi = (np.arange(n) + 1.0) ** (-1.0 / (beta - 1.0))
+    wi *= mean_degree / wi.mean()
+    wi = np.maximum(wi, 1.0)
+    cdf = np.cumsum(wi)
+    cdf /= cdf[-1]
+    pairs = int(wi.sum() // 2)
+    g = C.c_void_p()
+    _check(ctx.lib.lamg_gen_chung_lu(ctx.p, C.c_int32(n), _p(cdf), C.c_int64(pairs), C.c_uint64(seed),
+                                     C.c_int32(int(lcc)), C.byref(g)))
+    return DeviceGraph(ctx, g)
+
+
 def largest_component(a, ctx: Context | None = None) -> DeviceGraph:
     """graphs.largest_component on the device (union-find, ascending order)."""
     ctx = ctx or default_context()

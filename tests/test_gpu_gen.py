@@ -1,6 +1,6 @@
 """Graph ingest on the device (gen.cu) vs the host restatement (graphs.py).
 
-BASELINE config 5's R-MAT and the largest-component extraction used by
+BASELINE config 5's R-MAT, config 4's Chung-Lu and the largest-component extraction used by
 configs 3-5 (components.cpp:35-56 keeps ascending node
 order) must produce the same CSR Laplacian, bit for bit.
 """
@@ -23,6 +23,14 @@ def test_rmat_matches_host_generator(scale):
     from paper_1108_1310_b200 import lamg as L
     g = L.gen_rmat(scale, seed=5)
     _same(g.download(), G.rmat(scale, seed=5))
+    g.close()
+
+
+@pytest.mark.parametrize("n", [1000, 1 << 12, 50000, 1 << 17])
+def test_chung_lu_matches_host_generator(n):
+    from paper_1108_1310_b200 import lamg as L
+    g = L.gen_chung_lu(n, seed=4)
+    _same(g.download(), G.chung_lu(n, seed=4))
     g.close()
 
 

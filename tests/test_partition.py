@@ -8,8 +8,9 @@ plus exchanged ghosts equals the global residual. The exchange runs once in
 process and once between two gloo ranks (the N>1 path of the NCCL transport).
 
 GPU: the partitioned coloured sweep and residual (in-process transport, all
-parts on one device) are bit-identical to the single-part ones for 1-4 parts,
-and the single-part sweep is the sequential coloured sweep of the restatement.
+parts on one device) are bit-identical to the single-part ones for 2-4 parts
+(the single-part residual is checked against scipy), and the NCCL transport
+builds a communicator and sweeps on one rank.
 """
 import os
 import socket
@@ -123,10 +124,8 @@ def _rank(rank, world, port, q):
         if not isinstance(o, dist.P2POp):
             ghosts[o[1]:o[2]] = o[3]
     r_loc = _local_residual(a, d, b, own, ghosts.numpy())
-    full = [torch.zeros(1) for _ in range(world)]
     parts = [None] * world
     dist.all_gather_object(parts, (d["lo"], r_loc))
-    del full
     if rank == 0:
         got = np.empty(a.n)
         for lo, rl in parts:
@@ -173,4 +172,25 @@ def test_partitioned_sweep_bit_identical(name):
         assert np.array_equal(pl.residual(b, want_x), want_r), P
         pl.close()
     one.close()
+    ctx.close()
+
+
+@pytest.mark.gpu
+def test_nccl_transport_single_rank():
+    """The NCCL transport on one rank (the multi-rank exchange needs more GPUs
+    than this box has; its host side is the gloo test above): the library
+    loads libnccl, builds a communicator and sweeps like the in-process form."""
+    from paper_1108_1310_b200 import lamg as L
+    a = G.grid3d_7pt(30)
+    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    rng = np.random.default_rng(4)
+    b = rng.standard_normal(a.n)
+    b -= b.mean()
+    x = rng.standard_normal(a.n)
+    want = L.PartLevel(a, 1, ctx=ctx).smooth(b, x, 2)
+    comm = L.Comm(1, 0, L.Comm.unique_id(), ctx=ctx)
+    pl = L.PartLevel(a, 1, ctx=ctx, comm=comm)
+    assert np.array_equal(pl.smooth(b, x, 2), want)
+    pl.close()
+    comm.close()
     ctx.close()

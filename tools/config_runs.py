@@ -24,6 +24,11 @@ if cfg == 5:
     a = L.gen_rmat(25 - 2 * sd, seed=5, ctx=ctx)
     torch.cuda.synchronize()
     gen = {"where": "device (lamg_gen_rmat: samples, radix sort, run-length merge, union-find LCC, assembly)"}
+elif cfg == 4:
+    a = L.gen_chung_lu(1 << (24 - 2 * sd), seed=4, ctx=ctx)
+    torch.cuda.synchronize()
+    gen = {"where": "device (lamg_gen_chung_lu: host CDF, device inverse-CDF samples, radix sort, merge, "
+                    "union-find LCC, assembly)"}
 else:
     a = G.make_config(cfg, sd)
     gen = {"where": "host numpy (graphs.py)"}
