@@ -230,7 +230,17 @@ int lamg_part_plan(const lamg_csr *a, const int32_t *bounds, int32_t nparts, int
  * process owns parts [first_part, first_part + nown) */
 int lamg_part_level_create(lamg_ctx *ctx, const lamg_csr *a, const int32_t *bounds, int32_t nparts,
                            int32_t first_part, int32_t nown, lamg_comm *comm, lamg_part_level **out);
+/* the finest level of a hierarchy, partitioned (bounds by lamg_part_bounds) */
+int lamg_part_level_from_hier(lamg_ctx *ctx, const lamg_hier *h, int32_t nparts, int32_t first_part,
+                              int32_t nown, lamg_comm *comm, lamg_part_level **out);
 void lamg_part_level_destroy(lamg_part_level *pl);
+/* lamg_solve with the finest level partitioned (THROUGHPUT, flat cycle, finest
+ * level with an aggregation child): finest sweeps/residuals on the parts, the
+ * residual allgathered, coarse levels replicated on every rank; bit-identical
+ * to lamg_solve. b, x0, x: full host vectors (every rank passes all of b). */
+int lamg_part_solve(lamg_ctx *ctx, const lamg_hier *h, lamg_part_level *pl, const double *b, const double *x0,
+                    const lamg_cycle_cfg *cfg, double *x, lamg_solve_stats *stats, double *residuals,
+                    int32_t cap);
 /* global host vectors [n]: owned rows are read (b, x) and written (x, r) */
 int lamg_part_smooth(lamg_part_level *pl, const double *b, double *x, int32_t sweeps);
 int lamg_part_residual(lamg_part_level *pl, const double *b, const double *x, double *r);

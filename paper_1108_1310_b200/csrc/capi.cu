@@ -100,7 +100,7 @@ void upload_stage(Ctx& c, int32_t parent_n, int32_t coarse_n, int32_t nf, const 
 
 int solve_common(lamg_ctx* ctx, const lamg_hier* h, const double* b, const double* x0, bool dev,
                  const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
-                 int32_t cap) {
+                 int32_t cap, PartLevel* part = nullptr) {
   SolveResult res;
   int rc = guarded([&] {
     if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
@@ -115,14 +115,18 @@ int solve_common(lamg_ctx* ctx, const lamg_hier* h, const double* b, const doubl
       cc.target_reduction = cfg->target_reduction;
       cc.divergence_factor = cfg->divergence_factor;
     }
+    auto run = [&](const double* bb, const double* xx0, double* xx) {
+      return part ? solve_partitioned(c, *h->h, *part, bb, xx0, cc, xx, res)
+                  : solve_device(c, *h->h, bb, xx0, cc, xx, res);
+    };
     int r;
     if (dev) {
-      r = solve_device(c, *h->h, b, x0, cc, x, res);
+      r = run(b, x0, x);
     } else {
       DVec<double> db(n, c.s), dx0(n, c.s), dx(n, c.s);
       db.upload(b, n);
       dx0.upload(x0, n);
-      r = solve_device(c, *h->h, db.p, dx0.p, cc, dx.p, res);
+      r = run(db.p, dx0.p, dx.p);
       dx.download(x, n);
       c.sync();
     }
@@ -1142,6 +1146,43 @@ void lamg_part_level_destroy(lamg_part_level* pl) {
   if (!pl) return;
   cudaStreamSynchronize(pl->ctx->c.s);
   delete pl;
+}
+
+int lamg_part_level_from_hier(lamg_ctx* ctx, const lamg_hier* hier, int32_t nparts, int32_t first_part,
+                              int32_t nown, lamg_comm* comm, lamg_part_level** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!ctx || !hier || !hier->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    Ctx& c = ctx->c;
+    set_device(c);
+    const DCSR& op = hier->h->levels[0]->op;
+    std::vector<int64_t> rp = op.rp.to_host();
+    std::vector<int32_t> col(2 * op.m);
+    std::vector<double> val(2 * op.m), diag(op.n);
+    op.col.download(col.data(), 2 * op.m);
+    op.val.download(val.data(), 2 * op.m);
+    op.diag.download(diag.data(), op.n);
+    c.sync();
+    std::vector<int32_t> b;
+    part_bounds(op.n, rp.data(), nparts, b);
+    auto* h = new lamg_part_level();
+    h->ctx = ctx;
+    h->n = op.n;
+    try {
+      h->pl = std::make_unique<PartLevel>(c, op.view(), rp, col, val, diag, b, first_part, nown,
+                                          comm ? comm->c.get() : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int lamg_part_solve(lamg_ctx* ctx, const lamg_hier* h, lamg_part_level* pl, const double* b, const double* x0,
+                    const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals, int32_t cap) {
+  if (!pl) return guarded([] { throw LamgError(LAMG_E_ARGUMENT, "null partition"); });
+  return solve_common(ctx, h, b, x0, false, cfg, x, stats, residuals, cap, pl->pl.get());
 }
 
 int lamg_part_smooth(lamg_part_level* h, const double* b, double* x, int32_t sweeps) {

@@ -106,6 +106,7 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -123,11 +124,12 @@ NcclApi& nccl() {
     a.Recv = (decltype(a.Recv))dlsym(a.h, "ncclRecv");
     a.GroupStart = (decltype(a.GroupStart))dlsym(a.h, "ncclGroupStart");
     a.GroupEnd = (decltype(a.GroupEnd))dlsym(a.h, "ncclGroupEnd");
+    a.Broadcast = (decltype(a.Broadcast))dlsym(a.h, "ncclBroadcast");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(a.h, "ncclGetErrorString");
     return a;
   }();
   if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.GroupStart ||
-      !api.GroupEnd)
+      !api.GroupEnd || !api.Broadcast)
     throw LamgError(LAMG_E_NCCL, "libnccl.so.2 could not be loaded");
   return api;
 }
@@ -171,6 +173,11 @@ __global__ void take_kernel(const double* __restrict__ g, int32_t lo, int32_t cn
 __global__ void put_kernel(const double* __restrict__ l, int32_t lo, int32_t cnt, double* __restrict__ g) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) g[lo + i] = l[i];
+}
+__global__ void part_interp_kernel(double* __restrict__ x, const int32_t* __restrict__ agg, int32_t lo, int32_t n,
+                                   const double* __restrict__ xc) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = x[i] + xc[agg[lo + i]];
 }
 __global__ void local_perm_fill_kernel(const int64_t* rp, const int32_t* col, const double* val, const double* diag,
                                        const int32_t* rows, int32_t n, const int64_t* prp, int32_t* pcol,
@@ -386,6 +393,32 @@ void PartLevel::store(double* x_global_dev, double* r_global_dev) {
       count_launch(), put_kernel<<<blocks_for(pl.nloc), kThreads, 0, c.s>>>(p->r.p, pl.lo, pl.nloc, r_global_dev);
   }
   CK_LAUNCH();
+}
+
+void PartLevel::allgather(bool residual, double* full) {
+  if (!comm) {
+    store(residual ? nullptr : full, residual ? full : nullptr);
+    return;
+  }
+  Part& p = *parts[0];
+  NcclApi& api = nccl();
+  nck(api.GroupStart(), "ncclGroupStart");
+  for (int32_t q = 0; q < nparts(); ++q) {
+    const int32_t cnt = bounds[q + 1] - bounds[q];
+    if (!cnt) continue;
+    const double* src = q == comm->rank ? (residual ? p.r.p : p.x.p) : nullptr;
+    nck(api.Broadcast(src, full + bounds[q], cnt, ncclFloat64, q, (ncclComm_t)comm->handle, c.s), "ncclBroadcast");
+  }
+  nck(api.GroupEnd(), "ncclGroupEnd");
+}
+
+void PartLevel::interpolate(const int32_t* agg, const double* xc) {
+  for (auto& p : parts)
+    if (p->plan.nloc)
+      count_launch(), part_interp_kernel<<<blocks_for(p->plan.nloc), kThreads, 0, c.s>>>(p->x.p, agg, p->plan.lo,
+                                                                                      p->plan.nloc, xc);
+  CK_LAUNCH();
+  exchange();
 }
 
 }  // namespace lamgb

@@ -57,6 +57,21 @@ struct PartLevel {
   void residual();                 // r = b - A x on every owned part (ghosts current)
   void load(const double* b_global_dev, const double* x_global_dev);  // owned slices (+ exchange)
   void store(double* x_global_dev, double* r_global_dev);            // owned slices back
+  // every rank's owned slices into a full-size vector on every rank (x or r)
+  void allgather(bool residual, double* full_dev);
+  // x_local += xc[aggregate_of[global row]] for owned rows (add_interpolated), then exchange
+  void interpolate(const int32_t* aggregate_of_full, const double* xc);
 };
+
+// lamg::solve (cycle.cpp:221-273) with the finest level partitioned: the
+// finest sweeps and residuals run on the parts (halo exchange), the finest
+// residual is allgathered so every rank restricts it and runs the coarse
+// levels exactly as one device does (replicated, deterministic). THROUGHPUT,
+// flat cycle, finest level with an aggregation child. Bit-identical to
+// solve_device on one device.
+struct SolveResult;
+struct CycleCfg;
+int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, const double* x0, const CycleCfg& cfg,
+                      double* x, SolveResult& res);
 
 }  // namespace lamgb

@@ -12,6 +12,7 @@
 
 #include "batch.cuh"
 #include "solve.cuh"
+#include "part.cuh"
 
 namespace lamgb {
 
@@ -439,22 +440,15 @@ static std::string to_string_f(double v) {
   return buf;
 }
 
-// cycle.cpp:221-273; b, x0, x are device pointers of the finest size
-int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
-                 double* x, SolveResult& res) {
-  const DLevel& L0 = *h.levels[0];
-  const CSRv a = L0.op.view();
-  const int64_t n = a.n;
-  const bool exact = c.mode == LAMG_MODE_VALIDATE;
-  res = SolveResult{};
-  // compatibility: |sum b| <= 1e-10 ||b||_inf (sequential fold, exact max)
+// compatibility: |sum b| <= 1e-10 ||b||_inf (sequential fold, exact max); the
+// test is a threshold decision: sequential in VALIDATE mode (bit-exact with
+// the reference), fixed-order tree otherwise
+static void check_compatible(Ctx& c, const double* b, int64_t n, bool exact) {
   unsigned long long* bmax = (unsigned long long*)(c.dscal + 140);
   double* bsum = c.dscal + 141;
   CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), c.s));
   count_launch(), absmax_kernel<<<std::min(blocks_for(n), 1024), kThreads, 0, c.s>>>(b, n, bmax);
   CK_LAUNCH();
-  // the compatibility test is a threshold decision: sequential in VALIDATE
-  // mode (bit-exact with the reference), fixed-order tree otherwise
   if (exact) seq_sum(c, b, n, bsum);
   else tree_sum(c, b, n, bsum);
   CK(cudaMemcpyAsync(c.hscal, c.dscal + 140, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -467,7 +461,11 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   }
   if (std::fabs(b_sum) > 1e-10 * b_inf)
     throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
+}
 
+// THROUGHPUT data, workspace and the on-device tail of a one-column solve;
+// returns whether the tail runs the coarse levels
+static bool prepare_solve(Ctx& c, const DHier& h, const CycleCfg& cfg, bool exact) {
   if (!exact) const_cast<DHier&>(h).ensure_throughput([&] { prepare_throughput(c, const_cast<DHier&>(h)); });
   if (!c.ws) c.ws = new Workspace();
   Workspace& ws = *c.ws;
@@ -483,6 +481,20 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
   }
   if (!use_tail) ws.tail.first = 1 << 30;
   else ws.tail.reset(c);
+  return use_tail;
+}
+
+// cycle.cpp:221-273; b, x0, x are device pointers of the finest size
+int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
+                 double* x, SolveResult& res) {
+  const DLevel& L0 = *h.levels[0];
+  const CSRv a = L0.op.view();
+  const int64_t n = a.n;
+  const bool exact = c.mode == LAMG_MODE_VALIDATE;
+  res = SolveResult{};
+  check_compatible(c, b, n, exact);
+  const bool use_tail = prepare_solve(c, h, cfg, exact);
+  Workspace& ws = *c.ws;
   const double w0 = c.work = 0.0;
   // the solve runs on fixed-address copies of b and x (CUDA-graph replay)
   double* xw = ws.lv[0].x.p;
@@ -742,6 +754,114 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
   c.sync();
   for (int j = 0; j < nrhs; ++j)
     if (!res[j].message.empty()) return LAMG_E_DIVERGED;
+  return LAMG_OK;
+}
+
+
+// ------------------------------------------------ partitioned finest level
+// lamg::solve with the finest level split across parts (part.cuh). Level 0's
+// visit (cycle.cpp:176-209, theta = 1) runs its sweeps and residual on the
+// parts; the residual is allgathered so restrict_residual, the whole coarse
+// recursion (Driver::visit from level 1, tail included) and the coarse
+// correction are exactly the single-device ones on every rank; the
+// interpolation lands on the owned rows. Every kernel and fold order matches
+// solve_device, so the result is bit-identical to it.
+int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, const double* x0, const CycleCfg& cfg,
+                      double* x, SolveResult& res) {
+  const DLevel& L0 = *h.levels[0];
+  const int64_t n = L0.op.n;
+  res = SolveResult{};
+  if (c.mode != LAMG_MODE_THROUGHPUT || cfg.correction != 0)
+    throw LamgError(LAMG_E_ARGUMENT, "the partitioned solve runs THROUGHPUT mode with the flat cycle");
+  if (h.levels.size() < 2 || h.levels[1]->kind != KIND_AGG)
+    throw LamgError(LAMG_E_ARGUMENT, "the partitioned solve needs a finest level with an aggregation child");
+  if (pl.bounds.back() != n) throw LamgError(LAMG_E_DIMENSION_MISMATCH, "partition does not match the finest level");
+  check_compatible(c, b, n, false);
+  const bool use_tail = prepare_solve(c, h, cfg, false);
+  Workspace& ws = *c.ws;
+  const double w0 = c.work = 0.0;
+  double* xw = ws.lv[0].x.p;
+  double* bw = ws.lv[0].b.p;
+  double* rw = ws.lv[0].r.p;
+  copy_d(c, bw, b, n);
+  copy_d(c, xw, x0, n);
+  pl.load(bw, xw);
+  double* rn_d = c.dscal + 150;
+  double* growth = c.dscal + 151;
+  CK(cudaMemsetAsync(growth, 0, sizeof(double), c.s));
+  Driver d{c, h, cfg, ws, LevelCredits{}, false, growth};
+  d.credits.credit.assign(h.levels.size(), 0.0);
+  const double m0 = (double)L0.op.m;
+  auto residual_norm = [&] {
+    pl.residual();
+    c.work += m0;
+    pl.allgather(true, rw);
+    tree_norm2(c, rw, n, rn_d);
+  };
+  residual_norm();
+  const double r0 = read_scalar(c, rn_d);
+  res.residuals.push_back(r0);
+  const DLevel& child = *h.levels[1];
+  const DAgg& t = *child.agg;
+  LevelWS& wc = ws.lv[1];
+  if (r0 != 0.0) {
+    const double target = r0 / cfg.target_reduction;
+    for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
+      // visit(0, b, x, 1): one aggregation visit of the finest level
+      if (child.nu_pre) {
+        pl.sweep(child.nu_pre);
+        c.work += m0 * child.nu_pre;
+      }
+      pl.residual();
+      c.work += m0;
+      pl.allgather(true, rw);
+      restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, rw, cfg.mu, wc.b.p);
+      wc.x.zero();
+      const int theta_child = d.credits.take(1, child.gamma);
+      d.visit(1, wc.b.p, wc.x.p, theta_child);
+      pl.interpolate(t.aggregate_of.p, wc.x.p);
+      if (child.nu_post) {
+        pl.sweep(child.nu_post);
+        c.work += m0 * child.nu_post;
+      }
+      // subtract_mean over the whole iterate, then the cycle's residual
+      pl.allgather(false, xw);
+      subtract_mean_tree(c, xw, n);
+      pl.load(nullptr, xw);
+      residual_norm();
+      const double rn = read_scalar(c, rn_d);
+      res.residuals.push_back(rn);
+      res.cycles = cycle;
+      if (rn <= target) {
+        res.converged = true;
+        break;
+      }
+      if (rn > cfg.divergence_factor * r0 || !std::isfinite(rn)) {
+        res.acf = std::pow(rn / r0, 1.0 / cycle);
+        res.solve_work = (c.work - w0) / m0;
+        res.message = "solve diverged: residual grew from " + to_string_f(r0) + " to " + to_string_f(rn);
+        pl.allgather(false, xw);
+        copy_d(c, x, xw, n);
+        c.sync();
+        return LAMG_E_DIVERGED;
+      }
+    }
+  } else {
+    res.converged = true;
+  }
+  if (r0 == 0.0) {
+    subtract_mean_tree(c, xw, n);
+  } else {
+    pl.allgather(false, xw);
+    const double rp = res.residuals.back();
+    res.acf = std::pow(rp / r0, 1.0 / (double)res.cycles);
+  }
+  copy_d(c, x, xw, n);
+  if (use_tail) ws.tail.collect(c, &c.work, &d.relax_sweeps);
+  res.solve_work = (c.work - w0) / m0;
+  res.recombinations = d.recombinations;
+  res.recomb_max_growth = read_scalar(c, growth);
+  res.relax_sweeps = d.relax_sweeps;
   return LAMG_OK;
 }
 

@@ -783,6 +783,36 @@ class PartLevel:
                                                    C.c_int32(first), C.c_int32(nown),
                                                    comm.p if comm is not None else None, C.byref(self.p)))
 
+    @classmethod
+    def from_hierarchy(cls, h: Hierarchy, nparts: int, comm: Comm | None = None):
+        """The finest level of `h` split into `nparts` row blocks (lamg_part_level_from_hier)."""
+        self = cls.__new__(cls)
+        self.ctx, self.n = h.ctx, h.n
+        self.p = C.c_void_p()
+        first, nown = (0, nparts) if comm is None else (comm.rank, 1)
+        _check(self.ctx.lib.lamg_part_level_from_hier(self.ctx.p, h.h, C.c_int32(nparts), C.c_int32(first),
+                                                      C.c_int32(nown), comm.p if comm is not None else None,
+                                                      C.byref(self.p)))
+        return self
+
+    def solve(self, h: Hierarchy, b, x0, cfg: CycleConfig | None = None):
+        """lamg_part_solve: lamg::solve with this partitioned finest level."""
+        cfg = cfg or CycleConfig()
+        b, x0 = _f64(b), _f64(x0)
+        x = np.empty(self.n)
+        st = _lib.lamg_solve_stats()
+        cap = cfg.max_cycles + 2
+        res = np.empty(cap)
+        c = cfg.c()
+        code = self.ctx.lib.lamg_part_solve(self.ctx.p, h.h, self.p, _p(b), _p(x0), C.byref(c), _p(x), C.byref(st),
+                                            _p(res), C.c_int32(cap))
+        stats = SolveStats(list(res[:min(st.nresiduals, cap)]), st.acf, st.solve_work, st.cycles, bool(st.converged),
+                           st.recombinations, st.recomb_max_growth, st.relax_sweeps)
+        if code == 7:
+            raise DivergedError(_lib.lib().lamg_last_error().decode(), stats.as_dict())
+        _check(code)
+        return x, stats
+
     def smooth(self, b, x, sweeps: int = 1):
         b, x = _f64(b), _f64(x).copy()
         _check(self.ctx.lib.lamg_part_smooth(self.p, _p(b), _p(x), C.c_int32(sweeps)))

@@ -194,3 +194,27 @@ def test_nccl_transport_single_rank():
     pl.close()
     comm.close()
     ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["grid3d_48", "cfg2_128"])
+def test_partitioned_solve_bit_identical(name):
+    """lamg_part_solve: the finest level on 2-4 parts, coarse levels replicated
+    -- the iterate, the residual history and the cycle count equal lamg_solve's
+    bit for bit (THROUGHPUT), and the solve reaches the 1e-10 target."""
+    from paper_1108_1310_b200 import lamg as L
+    a = G.grid3d_7pt(48) if name == "grid3d_48" else G.make_config(2)
+    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    h = L.setup(a, ctx=ctx)
+    assert h.levels[1].kind == 2
+    b, x0 = G.gaussian_rhs(a.n, 17), G.default_x0(a.n)
+    x1, s1 = L.solve(h, b, x0, ctx=ctx)
+    assert s1.converged and s1.residuals[-1] <= s1.residuals[0] / 1e10
+    for P in ((2, 3) if name == "cfg2_128" else (1, 2, 4)):
+        pl = L.PartLevel.from_hierarchy(h, P)
+        xp, sp_ = pl.solve(h, b, x0)
+        assert sp_.cycles == s1.cycles, P
+        assert np.array_equal(np.array(sp_.residuals), np.array(s1.residuals)), P
+        assert np.array_equal(xp, x1), P
+        pl.close()
+    ctx.close()
