@@ -21,6 +21,20 @@ inline int bblocks(int64_t threads) { return (int)std::max<int64_t>(1, (threads 
 // lane, so the instruction count per row drops ~V-fold; each column is still
 // folded in entry order (same arithmetic as one thread per column).
 constexpr int kV = 4;
+// a thread's four columns of one node-major row: ONE 256-bit access on
+// sm_100 (LDG.E.ENL2.256 / STG.E.ENL2.256) instead of two 128-bit ones --
+// half the L1TEX requests of the gathers, which the block sweep is bound by
+struct d4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ d4 ld4(const double* p) {
+  d4 r;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
 template <int K, bool SUB>
 __device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict__ col,
                                       const double* __restrict__ val, const double* X, int64_t b, int64_t e, int k0) {
@@ -28,7 +42,7 @@ __device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict
   for (int64_t e0 = b; e0 < e; e0 += U) {
     int32_t c[U];
     double v[U];
-    double2 x01[U], x23[U];
+    d4 xv[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const bool ok = e0 + j < e;
@@ -37,32 +51,33 @@ __device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const double2* px = reinterpret_cast<const double2*>(X + (int64_t)c[j] * K + k0);
       const bool ok = e0 + j < e;
-      x01[j] = ok ? px[0] : make_double2(0.0, 0.0);
-      x23[j] = ok ? px[1] : make_double2(0.0, 0.0);
+      xv[j] = ok ? ld4(X + (int64_t)c[j] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
     }
 #pragma unroll
     for (int j = 0; j < U; ++j)
       if (e0 + j < e) {
         if (SUB) {
-          s[0] = s[0] - v[j] * x01[j].x;
-          s[1] = s[1] - v[j] * x01[j].y;
-          s[2] = s[2] - v[j] * x23[j].x;
-          s[3] = s[3] - v[j] * x23[j].y;
+          s[0] = s[0] - v[j] * xv[j].x;
+          s[1] = s[1] - v[j] * xv[j].y;
+          s[2] = s[2] - v[j] * xv[j].z;
+          s[3] = s[3] - v[j] * xv[j].w;
         } else {
-          s[0] = s[0] + v[j] * x01[j].x;
-          s[1] = s[1] + v[j] * x01[j].y;
-          s[2] = s[2] + v[j] * x23[j].x;
-          s[3] = s[3] + v[j] * x23[j].y;
+          s[0] = s[0] + v[j] * xv[j].x;
+          s[1] = s[1] + v[j] * xv[j].y;
+          s[2] = s[2] + v[j] * xv[j].z;
+          s[3] = s[3] + v[j] * xv[j].w;
         }
       }
   }
 }
 
 // one colour of the permuted operator; rows longer than kLongRow go to the long-row kernels
-template <int K>
-__global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+// 6 CTAs/SM (40 registers): the occupancy/in-flight-gathers optimum on the
+// cfg2 finest level (per colour: 1 CTA/SM bound -> 101 registers 464 us,
+// 6 -> 246 us, 8 -> spills 433 us)
+template <int K, int MINB = 6>
+__global__ void __launch_bounds__(kBT, MINB) bgs_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                   const double* __restrict__ val, const double* __restrict__ diag,
                                                   const int32_t* __restrict__ row_ids, int32_t i0, int32_t i1,
                                                   const double* __restrict__ B, double* X, const int32_t* done) {
@@ -74,9 +89,8 @@ __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp
   const int64_t b = __ldg(rp + i), e = __ldg(rp + i + 1);
   if (e - b > kLongRow) return;  // bgs_long_kernel / blong_*_kernel
   const int32_t u = __ldg(row_ids + i);
-  const double2* pb = reinterpret_cast<const double2*>(B + (int64_t)u * K + k0);
-  const double2 b01 = pb[0], b23 = pb[1];
-  double s[kV] = {b01.x, b01.y, b23.x, b23.y};
+  const d4 bv = ld4(B + (int64_t)u * K + k0);
+  double s[kV] = {bv.x, bv.y, bv.z, bv.w};
   fold4<K, true>(s, col, val, X, b, e, k0);
   const double d = __ldg(diag + i);
   double* px = X + (int64_t)u * K + k0;
@@ -85,8 +99,7 @@ __global__ void __launch_bounds__(kBT) bgs_kernel(const int64_t* __restrict__ rp
     for (int q = 0; q < kV; ++q)
       if (!done[k0 + q]) px[q] = s[q] / d;
   } else {
-    reinterpret_cast<double2*>(px)[0] = make_double2(s[0] / d, s[1] / d);
-    reinterpret_cast<double2*>(px)[1] = make_double2(s[2] / d, s[3] / d);
+    st4(px, s[0] / d, s[1] / d, s[2] / d, s[3] / d);
   }
 }
 
@@ -103,7 +116,7 @@ __device__ __forceinline__ void fold4_strided(double (&s)[kV], const int32_t* __
   for (int64_t base = j0; base < e; base += (int64_t)U * kSL) {
     int32_t c[U];
     double v[U];
-    double2 x01[U], x23[U];
+    d4 xv[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const int64_t j = base + (int64_t)q * kSL;
@@ -113,18 +126,16 @@ __device__ __forceinline__ void fold4_strided(double (&s)[kV], const int32_t* __
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const double2* px = reinterpret_cast<const double2*>(X + (int64_t)c[q] * K + k0);
       const bool ok = base + (int64_t)q * kSL < e;
-      x01[q] = ok ? px[0] : make_double2(0.0, 0.0);
-      x23[q] = ok ? px[1] : make_double2(0.0, 0.0);
+      xv[q] = ok ? ld4(X + (int64_t)c[q] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
     }
 #pragma unroll
     for (int q = 0; q < U; ++q)
       if (base + (int64_t)q * kSL < e) {
-        s[0] = s[0] + v[q] * x01[q].x;
-        s[1] = s[1] + v[q] * x01[q].y;
-        s[2] = s[2] + v[q] * x23[q].x;
-        s[3] = s[3] + v[q] * x23[q].y;
+        s[0] = s[0] + v[q] * xv[q].x;
+        s[1] = s[1] + v[q] * xv[q].y;
+        s[2] = s[2] + v[q] * xv[q].z;
+        s[3] = s[3] + v[q] * xv[q].w;
       }
   }
 }
@@ -199,8 +210,8 @@ __global__ void blong_fin_kernel(const int32_t* __restrict__ srows, const int32_
   }
 }
 
-template <int K>
-__global__ void __launch_bounds__(kBT) bres_kernel(CSRv a, const double* __restrict__ B, const double* __restrict__ X,
+template <int K, int MINB = 6>
+__global__ void __launch_bounds__(kBT, MINB) bres_kernel(CSRv a, const double* __restrict__ B, const double* __restrict__ X,
                                                    double* __restrict__ R) {
   constexpr int T = K / kV;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -210,15 +221,11 @@ __global__ void __launch_bounds__(kBT) bres_kernel(CSRv a, const double* __restr
   const int64_t b = __ldg(a.rp + u), e = __ldg(a.rp + u + 1);
   if (e - b > kLongRow) return;  // bres_long_kernel / blong_*_kernel
   const double d = __ldg(a.diag + u);
-  const double2* pxu = reinterpret_cast<const double2*>(X + u * K + k0);
-  const double2 x01 = pxu[0], x23 = pxu[1];
-  double s[kV] = {d * x01.x, d * x01.y, d * x23.x, d * x23.y};
+  const d4 xu = ld4(X + u * K + k0);
+  double s[kV] = {d * xu.x, d * xu.y, d * xu.z, d * xu.w};
   fold4<K, false>(s, a.col, a.val, X, b, e, k0);
-  const double2* pb = reinterpret_cast<const double2*>(B + u * K + k0);
-  const double2 b01 = pb[0], b23 = pb[1];
-  double2* pr = reinterpret_cast<double2*>(R + u * K + k0);
-  pr[0] = make_double2(b01.x - s[0], b01.y - s[1]);
-  pr[1] = make_double2(b23.x - s[2], b23.y - s[3]);
+  const d4 bv = ld4(B + u * K + k0);
+  st4(R + u * K + k0, bv.x - s[0], bv.y - s[1], bv.z - s[2], bv.w - s[3]);
 }
 
 template <int K>
