@@ -223,37 +223,80 @@ int32_t read_i32(Ctx& c, const int32_t* d) {
 // A left-to-right fold is one dependent chain of fp64 adds. One thread runs
 // it; loads are issued 32 at a time ahead of the chain (double-buffered) so
 // the chain, not memory latency, sets the pace.
+// Sequential folds of K <= 32 node-major columns (the reference's left-to-
+// right sums; bit-exact): three producer warps stream chunks of the input
+// into a shared-memory ring while lane k of warp 0 folds column k in row
+// order from shared memory. The dependent add chain, not the load latency,
+// sets the pace (the former single-thread loop waited ~0.6 us per 32 loads).
+constexpr int kFoldSlots = 4, kFoldSlot = 1024, kFoldThreads = 128;
 template <bool SQUARE>
-__global__ void seq_fold_kernel(const double* __restrict__ x, int64_t n, double* out) {
-  if (threadIdx.x != 0) return;
-  constexpr int B = 32;
-  double s = 0.0;
-  double cur[B], nxt[B];
-  int64_t base = 0;
-#pragma unroll
-  for (int j = 0; j < B; ++j) cur[j] = j < n ? x[j] : 0.0;
-  for (; base < n; base += B) {
-#pragma unroll
-    for (int j = 0; j < B; ++j) nxt[j] = base + B + j < n ? x[base + B + j] : 0.0;
-    const int cnt = n - base >= B ? B : (int)(n - base);
-    if (cnt == B) {
-#pragma unroll
-      for (int j = 0; j < B; ++j) s = s + (SQUARE ? cur[j] * cur[j] : cur[j]);
-    } else {
-      for (int j = 0; j < cnt; ++j) s = s + (SQUARE ? cur[j] * cur[j] : cur[j]);
+__global__ void __launch_bounds__(kFoldThreads) seq_cols_kernel(const double* __restrict__ x, int64_t n, int K,
+                                                                double* out, bool root) {
+  __shared__ double ring[kFoldSlots][kFoldSlot];
+  __shared__ int produced, consumed;
+  const int64_t rows_per = kFoldSlot / K;
+  const int64_t nchunks = (n + rows_per - 1) / rows_per;
+  if (threadIdx.x == 0) produced = consumed = 0;
+  __syncthreads();
+  volatile int* vp = &produced;
+  volatile int* vc = &consumed;
+  if (threadIdx.x >= 32) {
+    const int pt = threadIdx.x - 32, np = kFoldThreads - 32;
+    for (int64_t k = 0; k < nchunks; ++k) {
+      while (k - *vc >= kFoldSlots) {
+      }
+      const int64_t r0 = k * rows_per;
+      const int64_t cnt = (n - r0 < rows_per ? n - r0 : rows_per) * K;
+      double* slot = ring[k % kFoldSlots];
+      const double* src = x + r0 * K;
+      for (int64_t j = pt; j < cnt; j += np) slot[j] = __ldcs(src + j);
+      __threadfence_block();
+      asm volatile("bar.sync 1, %0;" ::"r"(np) : "memory");
+      if (pt == 0) *vp = (int)(k + 1);
     }
-#pragma unroll
-    for (int j = 0; j < B; ++j) cur[j] = nxt[j];
+    return;
   }
-  *out = SQUARE ? sqrt(s) : s;
+  const int lane = threadIdx.x;
+  double s = 0.0;
+  for (int64_t k = 0; k < nchunks; ++k) {
+    while (*vp <= k) {
+    }
+    __threadfence_block();
+    const int64_t r0 = k * rows_per;
+    const int rows = (int)(n - r0 < rows_per ? n - r0 : rows_per);
+    if (lane < K) {
+      const double* slot = ring[k % kFoldSlots] + lane;
+      int i = 0;
+      for (; i + 8 <= rows; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = slot[(i + j) * K];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s = s + (SQUARE ? v[j] * v[j] : v[j]);
+      }
+      for (; i < rows; ++i) {
+        const double v = slot[i * K];
+        s = s + (SQUARE ? v * v : v);
+      }
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) *vc = (int)(k + 1);
+  }
+  if (lane < K) out[lane] = root ? sqrt(s) : s;
 }
 
 void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
-  count_launch(), seq_fold_kernel<false><<<1, 32, 0, c.s>>>(x, n, d_out);
+  count_launch(), seq_cols_kernel<false><<<1, kFoldThreads, 0, c.s>>>(x, n, 1, d_out, false);
   CK_LAUNCH();
 }
 void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
-  count_launch(), seq_fold_kernel<true><<<1, 32, 0, c.s>>>(x, n, d_out);
+  count_launch(), seq_cols_kernel<true><<<1, kFoldThreads, 0, c.s>>>(x, n, 1, d_out, true);
+  CK_LAUNCH();
+}
+void seq_col_sums(Ctx& c, const double* x, int64_t n, int K, double* d_out) {
+  if (K < 1 || K > 32) throw LamgError(LAMG_E_ARGUMENT, "sequential column sums take 1..32 columns");
+  count_launch(), seq_cols_kernel<false><<<1, kFoldThreads, 0, c.s>>>(x, n, K, d_out, false);
   CK_LAUNCH();
 }
 

@@ -425,6 +425,8 @@ int32_t reduce_max_i32(Ctx& c, const int32_t* in, int64_t n);
 void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out);
 // out = sqrt(sum x_i^2) with the same fold order (norm2, sparse_laplacian.cpp:236-240)
 void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out);
+// sums of the K <= 32 columns of a node-major [n][K] block, each in row order (bit-exact)
+void seq_col_sums(Ctx& c, const double* x, int64_t n, int K, double* d_out);
 // fixed-order tree reductions (throughput mode)
 void tree_sum(Ctx& c, const double* x, int64_t n, double* d_out);
 void tree_norm2(Ctx& c, const double* x, int64_t n, double* d_out);

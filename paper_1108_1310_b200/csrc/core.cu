@@ -321,14 +321,6 @@ void fill_pm1(Ctx& c, double* x, int64_t n, uint64_t seed, int stride, int offse
 }
 
 // ------------------------------------------------------- mean subtraction
-// K columns folded independently, one lane per column, rows in order
-__global__ void col_seq_sum_kernel(const double* __restrict__ x, int64_t n, int K, double* sums) {
-  int k = threadIdx.x;
-  if (k >= K) return;
-  double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s = s + x[i * K + k];
-  sums[k] = s;
-}
 __global__ void sub_mean_kernel(double* x, int64_t n, int K, const double* sums) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n * K) return;
@@ -342,8 +334,7 @@ void subtract_mean_seq(Ctx& c, double* x, int64_t n, int K) {
   double* sums = c.dscal + 64;  // [64..80)
   if (K == 1) seq_sum(c, x, n, sums);
   else {
-    count_launch(), col_seq_sum_kernel<<<1, 32, 0, c.s>>>(x, n, K, sums);
-    CK_LAUNCH();
+    seq_col_sums(c, x, n, K, sums);
   }
   count_launch(), sub_mean_kernel<<<blocks_for(n * K), kThreads, 0, c.s>>>(x, n, K, sums);
   CK_LAUNCH();
