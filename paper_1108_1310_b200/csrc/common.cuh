@@ -364,6 +364,40 @@ __device__ __forceinline__ double block_dot(const int32_t* __restrict__ col, con
   return sh_bd[32];
 }
 
+// VALIDATE-mode long row by one warp: s (-|+)= val[k]*x[col[k]] for k in
+// [b,e) in k order, bit-identical to the sequential loop. Lanes form 32
+// products at a time (each rounded exactly as in the loop); every lane then
+// runs the same add chain over the shuffled products, so all lanes hold s.
+// The next 32 products are loaded before the current chain runs.
+template <bool SUB>
+__device__ __forceinline__ double warp_seq_fold(double s, const int32_t* __restrict__ col,
+                                                const double* __restrict__ val, const double* x, int64_t b,
+                                                int64_t e, int xs = 1, int xk = 0) {
+  const int lane = threadIdx.x & 31;
+  int64_t k = b + lane;
+  double p = k < e ? val[k] * x[(int64_t)col[k] * xs + xk] : 0.0;
+  for (int64_t c0 = b; c0 < e; c0 += 32) {
+    const int64_t kn = c0 + 32 + lane;
+    const double pn = kn < e ? val[kn] * x[(int64_t)col[kn] * xs + xk] : 0.0;
+    const int cnt = e - c0 < 32 ? (int)(e - c0) : 32;
+    if (cnt == 32) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double pj = __shfl_sync(0xffffffffu, p, j);
+        s = SUB ? s - pj : s + pj;
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const double pj = __shfl_sync(0xffffffffu, p, j);
+        s = SUB ? s - pj : s + pj;
+      }
+    }
+    p = pn;
+  }
+  return s;
+}
+constexpr int64_t kWarpRowExact = 64;  // exact folds of longer rows take a warp
+
 // VALIDATE-mode heavy row: s (-|+)= val[k]*x[col[k]] for k in [b,e) in k
 // order, bit-identical to the sequential loop. The CTA computes the products
 // (each rounded exactly as in the loop) in parallel chunks through shared

@@ -204,10 +204,31 @@ __global__ void gs_fronts_kernel(CSRv a, const double* __restrict__ b, double* x
           }
         }
       }
+      // long rows of this front: a warp each (exact chain over shuffled products);
+      // blockDim is a multiple of K, so only its full warps take part
+      const int nfw = blockDim.x >> 5;
+      const int64_t gw = (int64_t)blockIdx.x * nfw + (threadIdx.x >> 5);
+      const bool full_warp = (int)(threadIdx.x >> 5) < nfw;
+      for (int64_t i = fs + gw; full_warp && i < fe; i += (int64_t)gridDim.x * nfw) {
+        const int32_t u = rows[i];
+        const int64_t len = a.rp[u + 1] - a.rp[u];
+        if (len <= kWarpRowExact || len > kHeavyRowExact) continue;
+        const double d = a.diag[u];
+        for (int kk = 0; kk < K; ++kk) {
+          const double s = warp_seq_fold<true>(b ? b[(int64_t)u * K + kk] : 0.0, a.col, a.val, x, a.rp[u],
+                                               a.rp[u + 1], K, kk);
+          if ((threadIdx.x & 31) == 0) {
+            if (d != 0.0) x[(int64_t)u * K + kk] = s / d;
+            else
+              dev_report(err, backward ? (unsigned long long)(a.n - 1 - u) : (unsigned long long)u,
+                         DE_GS_SINGULAR, u, 0);
+          }
+        }
+      }
       for (int64_t i = fs + gtid / K; i < fe; i += gstride / K) {
         const int kk = (int)(gtid % K);
         const int32_t u = rows[i];
-        if (a.rp[u + 1] - a.rp[u] > kHeavyRowExact) continue;
+        if (a.rp[u + 1] - a.rp[u] > kWarpRowExact) continue;
         double s = b ? b[(int64_t)u * K + kk] : 0.0;
         const int64_t e = a.rp[u + 1];
         if (K == 1) s = row_fold<8, true>(s, a.col, a.val, x, a.rp[u], e);
