@@ -408,22 +408,32 @@ template <bool SUB>
 __device__ __forceinline__ double block_seq_fold(double s, const int32_t* __restrict__ col,
                                                  const double* __restrict__ val, const double* x, int64_t b,
                                                  int64_t e, int xs = 1, int xk = 0) {
-  __shared__ double sh_prod[256];
+  // double-buffered: while thread 0 runs the add chain over chunk q, the CTA
+  // forms the products of chunk q + 1, so an iteration costs the longer of
+  // the two instead of their sum (1024-entry chunks: the chain dominates)
+  constexpr int C = 1024;
+  __shared__ double sh_prod[2][C];
   __shared__ double sh_s;
   if (threadIdx.x == 0) sh_s = s;
-  for (int64_t c0 = b; c0 < e; c0 += 256) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < 256; j += blockDim.x) {
+  auto fill = [&](int buf, int64_t c0) {
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
       const int64_t k = c0 + j;
-      sh_prod[j] = k < e ? (x ? val[k] * x[(int64_t)col[k] * xs + xk] : val[k]) : 0.0;
+      sh_prod[buf][j] = k < e ? (x ? val[k] * x[(int64_t)col[k] * xs + xk] : val[k]) : 0.0;
     }
-    __syncthreads();
+  };
+  __syncthreads();
+  if (b < e) fill(0, b);
+  int buf = 0;
+  for (int64_t c0 = b; c0 < e; c0 += C) {
+    __syncthreads();  // chunk c0 is in sh_prod[buf]; the other buffer is free
+    if (c0 + C < e) fill(buf ^ 1, c0 + C);
     if (threadIdx.x == 0) {
-      const int cnt = e - c0 < 256 ? (int)(e - c0) : 256;
+      const int cnt = e - c0 < C ? (int)(e - c0) : C;
       double t = sh_s;
-      for (int j = 0; j < cnt; ++j) t = SUB ? t - sh_prod[j] : t + sh_prod[j];
+      for (int j = 0; j < cnt; ++j) t = SUB ? t - sh_prod[buf][j] : t + sh_prod[buf][j];
       sh_s = t;
     }
+    buf ^= 1;
   }
   __syncthreads();
   const double r = sh_s;

@@ -83,8 +83,20 @@ __global__ void kahn_kernel(CSRv a, bool backward, int32_t* cnt, int32_t* level,
   const int lane = threadIdx.x & 31;
   int32_t fs = 0, fe = first_count, r = 0;
   while (fs < fe) {
+    // hubs (over kHeavyRowExact entries) release their neighbours with a whole CTA
+    for (int64_t i = fs + blockIdx.x; i < fe; i += gridDim.x) {
+      const int32_t u = queue[i];
+      if (a.rp[u + 1] - a.rp[u] <= kHeavyRowExact) continue;
+      if (threadIdx.x == 0) level[u] = r;
+      for (int64_t k = a.rp[u] + threadIdx.x; k < a.rp[u + 1]; k += blockDim.x) {
+        const int32_t v = a.col[k];
+        const bool later = backward ? (v < u) : (v > u);
+        if (later && atomicSub(&cnt[v], 1) == 1) queue[atomicAdd(&ctl[0], 1)] = v;
+      }
+    }
     for (int64_t i = fs + gwarp; i < fe; i += nwarps) {
       int32_t u = queue[i];
+      if (a.rp[u + 1] - a.rp[u] > kHeavyRowExact) continue;
       if (lane == 0) level[u] = r;
       for (int64_t k = a.rp[u] + lane; k < a.rp[u + 1]; k += 32) {
         int32_t v = a.col[k];

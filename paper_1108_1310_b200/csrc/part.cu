@@ -351,12 +351,7 @@ void PartLevel::exchange() {
 void PartLevel::sweep(int sweeps) {
   for (int s = 0; s < sweeps; ++s)
     for (int32_t cc = 0; cc < ncolors; ++cc) {
-      bool any = false;
-      for (auto& p : parts) {
-        if (p->color.cptr_h[cc + 1] > p->color.cptr_h[cc]) any = true;
-        gs_colored_one(c, p->color, p->b.p, p->x.p, cc);
-      }
-      (void)any;
+      for (auto& p : parts) gs_colored_one(c, p->color, p->b.p, p->x.p, cc);
       exchange();  // the next colour reads this colour's new values across blocks
     }
 }
