@@ -42,6 +42,8 @@ enum {
   LAMG_E_DIMENSION_MISMATCH = 5, /* lamg::DimensionMismatchError */
   LAMG_E_INCOMPATIBLE_RHS = 6,   /* lamg::IncompatibleRhsError */
   LAMG_E_DIVERGED = 7,           /* lamg::DivergedError (stats still filled) */
+  LAMG_E_PARSE = 8,              /* lamg::ParseError */
+  LAMG_E_IO = 9,                 /* lamg::IoError */
   LAMG_E_CUDA = 10,
   LAMG_E_NCCL = 11,
   LAMG_E_ARGUMENT = 12
@@ -246,6 +248,18 @@ int lamg_part_smooth(lamg_part_level *pl, const double *b, double *x, int32_t sw
 int lamg_part_residual(lamg_part_level *pl, const double *b, const double *x, double *r);
 /* device-resident timing of `sweeps` partitioned sweeps (+ one residual) */
 int lamg_part_time(lamg_part_level *pl, int32_t sweeps, float *ms);
+
+/* ---- Matrix Market files (matrix_market.hpp:34-52): read_matrix_market_file
+ * + assemble_problem -> a host CSR Laplacian, and write_matrix_market_file.
+ * kind: 0 auto, 1 adjacency, 2 laplacian. Lines are parsed by all host
+ * threads; the assembled CSR and warnings equal the reference's. ----------- */
+typedef struct lamg_mm lamg_mm;
+int lamg_mm_read(const char *path, int32_t kind, int32_t absolute_weight_policy, lamg_mm **out);
+int lamg_mm_info(const lamg_mm *mm, int32_t *n, int64_t *m, int32_t *was_laplacian, int32_t *nwarnings);
+int lamg_mm_warning(const lamg_mm *mm, int32_t i, char *buf, int32_t cap);
+int lamg_mm_csr(const lamg_mm *mm, int64_t *row_ptr, int32_t *col, double *val, double *diag);
+void lamg_mm_destroy(lamg_mm *mm);
+int lamg_mm_write(const char *path, const lamg_csr *a, int32_t as_laplacian);
 
 /* ---- kernel timing (bench roofline): CUDA events around the finest-level
  * residual and Gauss-Seidel launches of the solves issued on ctx ---------- */

@@ -67,6 +67,7 @@ def lib():
         L.lamg_graph_destroy.restype = None
         L.lamg_comm_destroy.restype = None
         L.lamg_part_level_destroy.restype = None
+        L.lamg_mm_destroy.restype = None
         _lib = L
     return _lib
 

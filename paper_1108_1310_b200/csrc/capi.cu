@@ -9,6 +9,7 @@
 
 #include "batch.cuh"
 #include "part.cuh"
+#include "mmio.cuh"
 #include "solve.cuh"
 
 using namespace lamgb;
@@ -1229,6 +1230,66 @@ int lamg_part_time(lamg_part_level* h, int32_t sweeps, float* ms) {
     CK(cudaEventElapsedTime(ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+// ------------------------------------------------------ Matrix Market files
+struct lamg_mm {
+  MMProblem p;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> col;
+  std::vector<double> val, diag;
+};
+
+int lamg_mm_read(const char* path, int32_t kind, int32_t absolute_weight_policy, lamg_mm** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (!path) throw LamgError(LAMG_E_ARGUMENT, "null path");
+    auto* mm = new lamg_mm();
+    try {
+      mm->p = read_matrix_market_file(path, kind, absolute_weight_policy != 0);
+      assemble_problem(mm->p, mm->rp, mm->col, mm->val, mm->diag);
+    } catch (...) {
+      delete mm;
+      throw;
+    }
+    *out = mm;
+  });
+}
+
+int lamg_mm_info(const lamg_mm* mm, int32_t* n, int64_t* m, int32_t* was_laplacian, int32_t* nwarnings) {
+  return guarded([&] {
+    if (!mm) throw LamgError(LAMG_E_ARGUMENT, "null problem");
+    *n = mm->p.n;
+    *m = (int64_t)mm->p.edges.size();
+    *was_laplacian = mm->p.was_laplacian ? 1 : 0;
+    *nwarnings = (int32_t)mm->p.warnings.size();
+  });
+}
+
+int lamg_mm_warning(const lamg_mm* mm, int32_t i, char* buf, int32_t cap) {
+  return guarded([&] {
+    if (!mm || i < 0 || i >= (int32_t)mm->p.warnings.size()) throw LamgError(LAMG_E_ARGUMENT, "no such warning");
+    snprintf(buf, cap, "%s", mm->p.warnings[i].c_str());
+  });
+}
+
+int lamg_mm_csr(const lamg_mm* mm, int64_t* row_ptr, int32_t* col, double* val, double* diag) {
+  return guarded([&] {
+    if (!mm) throw LamgError(LAMG_E_ARGUMENT, "null problem");
+    if (row_ptr) memcpy(row_ptr, mm->rp.data(), sizeof(int64_t) * mm->rp.size());
+    if (col) memcpy(col, mm->col.data(), sizeof(int32_t) * mm->col.size());
+    if (val) memcpy(val, mm->val.data(), sizeof(double) * mm->val.size());
+    if (diag) memcpy(diag, mm->diag.data(), sizeof(double) * mm->diag.size());
+  });
+}
+
+void lamg_mm_destroy(lamg_mm* mm) { delete mm; }
+
+int lamg_mm_write(const char* path, const lamg_csr* a, int32_t as_laplacian) {
+  return guarded([&] {
+    if (!path || !a) throw LamgError(LAMG_E_ARGUMENT, "null argument");
+    write_matrix_market_file(path, a->n, a->m, a->row_ptr, a->col, a->val, a->diag, as_laplacian != 0);
   });
 }
 

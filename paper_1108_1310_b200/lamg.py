@@ -70,9 +70,17 @@ class CudaError(Error):
     kind = "CudaError"
 
 
+class ParseError(Error):
+    kind = "ParseError"
+
+
+class IoError(Error):
+    kind = "IoError"
+
+
 _CODES = {1: Error, 2: EmptyGraphError, 3: SingularDiagonalError, 4: InvalidLaplacianError,
-          5: DimensionMismatchError, 6: IncompatibleRhsError, 7: DivergedError, 10: CudaError,
-          11: Error, 12: Error}
+          5: DimensionMismatchError, 6: IncompatibleRhsError, 7: DivergedError, 8: ParseError, 9: IoError,
+          10: CudaError, 11: Error, 12: Error}
 
 
 def _check(code: int):
@@ -840,3 +848,40 @@ class PartLevel:
         except Exception:  # noqa: BLE001
             pass
 
+
+
+# ------------------------------------------------------------ Matrix Market
+_MM_KIND = {"auto": 0, "adjacency": 1, "laplacian": 2}
+
+
+def read_matrix_market(path: str, kind: str = "auto", absolute_weight_policy: bool = True):
+    """read_matrix_market_file + assemble_problem (matrix_market.hpp:34-45).
+
+    Returns (SparseLaplacian, was_laplacian, warnings). Host only.
+    """
+    lib = _lib.lib()
+    mm = C.c_void_p()
+    _check(lib.lamg_mm_read(str(path).encode(), C.c_int32(_MM_KIND[kind]), C.c_int32(int(absolute_weight_policy)),
+                            C.byref(mm)))
+    try:
+        n, m, wl, nw = C.c_int32(), C.c_int64(), C.c_int32(), C.c_int32()
+        _check(lib.lamg_mm_info(mm, C.byref(n), C.byref(m), C.byref(wl), C.byref(nw)))
+        rp = np.empty(n.value + 1, np.int64)
+        col = np.empty(2 * m.value, np.int32)
+        val = np.empty(2 * m.value)
+        diag = np.empty(n.value)
+        _check(lib.lamg_mm_csr(mm, _p(rp), _p(col), _p(val), _p(diag)))
+        warnings = []
+        for i in range(nw.value):
+            buf = C.create_string_buffer(1024)
+            _check(lib.lamg_mm_warning(mm, C.c_int32(i), buf, C.c_int32(1024)))
+            warnings.append(buf.value.decode())
+        return SparseLaplacian(n.value, m.value, rp, col, val, diag), bool(wl.value), warnings
+    finally:
+        lib.lamg_mm_destroy(mm)
+
+
+def write_matrix_market(path: str, a, as_laplacian: bool = False):
+    """write_matrix_market_file (matrix_market.hpp:47-52)."""
+    arg = _CSRArg(a)
+    _check(_lib.lib().lamg_mm_write(str(path).encode(), arg.ref(), C.c_int32(int(as_laplacian))))
