@@ -762,7 +762,7 @@ int lamg_k_probe(lamg_ctx* ctx, const lamg_csr* a, int32_t sweeps, uint64_t seed
     build_schedule(c, av, false, sch);
     UpperIndex upi;
     build_upper_index(c, av, upi);
-    *factor = probe_relaxation(c, av, sch, upi, sweeps, seed);
+    *factor = probe_factor(c, av, sch, upi, sweeps, seed, true);  // the value, bit for bit
   });
 }
 

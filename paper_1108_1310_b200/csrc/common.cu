@@ -231,7 +231,7 @@ int32_t read_i32(Ctx& c, const int32_t* d) {
 constexpr int kFoldSlots = 4, kFoldSlot = 1024, kFoldThreads = 128;
 template <bool SQUARE>
 __global__ void __launch_bounds__(kFoldThreads) seq_cols_kernel(const double* __restrict__ x, int64_t n, int K,
-                                                                double* out, bool root) {
+                                                                double* out, bool root, bool debug = false) {
   __shared__ double ring[kFoldSlots][kFoldSlot];
   __shared__ int produced, consumed;
   const int64_t rows_per = kFoldSlot / K;
@@ -243,8 +243,12 @@ __global__ void __launch_bounds__(kFoldThreads) seq_cols_kernel(const double* __
   if (threadIdx.x >= 32) {
     const int pt = threadIdx.x - 32, np = kFoldThreads - 32;
     for (int64_t k = 0; k < nchunks; ++k) {
-      while (k - *vc >= kFoldSlots) {
-      }
+      // one producer polls the ring (96 spinning threads would steal the
+      // consumer's shared-memory bandwidth), the others wait at the barrier
+      if (pt == 0)
+        while (k - *vc >= kFoldSlots) {
+        }
+      asm volatile("bar.sync 1, %0;" ::"r"(np) : "memory");
       const int64_t r0 = k * rows_per;
       const int64_t cnt = (n - r0 < rows_per ? n - r0 : rows_per) * K;
       double* slot = ring[k % kFoldSlots];
@@ -258,21 +262,24 @@ __global__ void __launch_bounds__(kFoldThreads) seq_cols_kernel(const double* __
   }
   const int lane = threadIdx.x;
   double s = 0.0;
+  long long t_wait = 0, t_all = clock64();
   for (int64_t k = 0; k < nchunks; ++k) {
+    const long long tw = clock64();
     while (*vp <= k) {
     }
+    t_wait += clock64() - tw;
     __threadfence_block();
     const int64_t r0 = k * rows_per;
     const int rows = (int)(n - r0 < rows_per ? n - r0 : rows_per);
     if (lane < K) {
       const double* slot = ring[k % kFoldSlots] + lane;
       int i = 0;
-      for (; i + 8 <= rows; i += 8) {
-        double v[8];
+      for (; i + 16 <= rows; i += 16) {
+        double v[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = slot[(i + j) * K];
+        for (int j = 0; j < 16; ++j) v[j] = slot[(i + j) * K];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s = s + (SQUARE ? v[j] * v[j] : v[j]);
+        for (int j = 0; j < 16; ++j) s = s + (SQUARE ? v[j] * v[j] : v[j]);
       }
       for (; i < rows; ++i) {
         const double v = slot[i * K];
@@ -284,10 +291,12 @@ __global__ void __launch_bounds__(kFoldThreads) seq_cols_kernel(const double* __
     if (lane == 0) *vc = (int)(k + 1);
   }
   if (lane < K) out[lane] = root ? sqrt(s) : s;
+  if (debug && lane == 0) printf("[fold] n %lld K %d cycles %lld waiting %lld\n", (long long)n, K, clock64() - t_all, t_wait);
 }
 
 void seq_sum(Ctx& c, const double* x, int64_t n, double* d_out) {
-  count_launch(), seq_cols_kernel<false><<<1, kFoldThreads, 0, c.s>>>(x, n, 1, d_out, false);
+  static const bool dbg = getenv("LAMG_FOLD_DEBUG") != nullptr;
+  count_launch(), seq_cols_kernel<false><<<1, kFoldThreads, 0, c.s>>>(x, n, 1, d_out, false, dbg);
   CK_LAUNCH();
 }
 void seq_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {

@@ -333,6 +333,19 @@ void energy_seq(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, do
   seq_sum(c, scratch.p, up.count, d_out);
 }
 
+// the same energy with a fixed-order tree sum of the terms (probe fast path)
+void energy_tree(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, double* d_out,
+                 DVec<double>& scratch) {
+  if (scratch.n < up.count) scratch.alloc(up.count, c.s);
+  if (up.count == 0) {
+    CK(cudaMemsetAsync(d_out, 0, sizeof(double), c.s));
+    return;
+  }
+  count_launch(), energy_terms_kernel<<<blocks_for(up.count), kThreads, 0, c.s>>>(a, up.entry.p, up.row.p, up.count, x, scratch.p);
+  CK_LAUNCH();
+  tree_sum(c, scratch.p, up.count, d_out);
+}
+
 // -------------------------------------------------------------------- rng
 __device__ inline uint64_t splitmix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;

@@ -53,6 +53,8 @@ void build_upper_index(Ctx& c, const CSRv& a, UpperIndex& out);
 constexpr int64_t kHeavyRowExact = 2048;
 void energy_seq(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, double* d_out,
                 DVec<double>& scratch);
+void energy_tree(Ctx& c, const CSRv& a, const UpperIndex& up, const double* x, double* d_out,
+                DVec<double>& scratch);
 
 // x[i] = Rng(seed) draw i in [-1,1) (rng.hpp:31), counter form; stride/offset
 // place it into a node-major block

@@ -193,6 +193,9 @@ bool eliminate_rounds(Ctx& c, const CSRv& a, std::vector<std::unique_ptr<DStage>
                       DCSR& coarse);
 double probe_relaxation(Ctx& c, const CSRv& a, const Schedule& sch, const UpperIndex& up,
                         int sweeps, uint64_t seed);
+// the factor itself with the reference's sequential folds (parity harness)
+double probe_factor(Ctx& c, const CSRv& a, const Schedule& sch, const UpperIndex& up, int sweeps, uint64_t seed,
+                    bool exact);
 void generate_tvs(Ctx& c, const CSRv& a, const Schedule& sch, int K, int sweeps, uint64_t seed,
                   DVec<double>& X /* n*K node-major */);
 void compute_affinities(Ctx& c, const CSRv& a, int K, const double* X, double* aff, double* nn);
