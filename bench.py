@@ -472,7 +472,7 @@ def main():
     ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-cycles", type=int, default=3)
-    ap.add_argument("--lanes", type=int, default=6, help="concurrent solve lanes (contexts/streams) per GPU")
+    ap.add_argument("--lanes", type=int, default=8, help="concurrent solve lanes (contexts/streams) per GPU")
     ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..32; 1 = single solves)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")
