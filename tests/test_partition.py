@@ -192,6 +192,14 @@ def test_nccl_transport_single_rank():
     pl = L.PartLevel(a, 1, ctx=ctx, comm=comm)
     assert np.array_equal(pl.smooth(b, x, 2), want)
     pl.close()
+    # the partitioned solve over the NCCL transport (allgathers by ncclBroadcast)
+    h = L.setup(a, ctx=ctx)
+    bb, x0 = G.gaussian_rhs(a.n, 5), G.default_x0(a.n)
+    x1, s1 = L.solve(h, bb, x0, ctx=ctx)
+    ps = L.PartLevel.from_hierarchy(h, 1, comm=comm)
+    xp, sp_ = ps.solve(h, bb, x0)
+    assert sp_.cycles == s1.cycles and np.array_equal(xp, x1)
+    ps.close()
     comm.close()
     ctx.close()
 
