@@ -297,6 +297,9 @@ void lamg_ctx_destroy(lamg_ctx* ctx) {
   c.bws = nullptr;
   c.bscratch.release();
   c.rpart.release();
+  c.rcnt.release();
+  if (c.relax_graph.exec) cudaGraphExecDestroy(c.relax_graph.exec);
+  c.relax_graph.exec = nullptr;
   c.ripart.release();
   c.rcptr.release();
   c.rtpart.release();

@@ -209,7 +209,19 @@ struct Ctx {
   double* dbscal = nullptr;     // batched scalars (256 doubles)
   int32_t* dbdone = nullptr;    // batched per-column masks (64 ints)
   DVec<double> bscratch;        // batched long-row chunk sums (grown on demand)
+  // relaxation / task residual scratch, per context so concurrent solves over
+  // one hierarchy never share it; rgen changes whenever a buffer moves (it
+  // keys the cached sweep graph)
   DVec<double> rpart, ripart;   // cooperative relaxation: block partials, chunk partials
+  DVec<uint32_t> rcnt;          // chunk counters of super-long rows (return to 0 after each row)
+  int64_t rgen = 0;
+  struct RelaxGraph {
+    const void* key = nullptr;  // the DColor
+    const void *b = nullptr, *x = nullptr, *r = nullptr;
+    int64_t gen = -1;
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+  } relax_graph;
   DVec<int32_t> rcptr;          // cooperative relaxation: natural-order range {0, n}
   DVec<double> rtpart;          // residual_tasks: chunk partials
   DVec<int32_t> rtcptr;         // residual_tasks: {0, n} of the last operator

@@ -75,7 +75,6 @@ struct LongRows {
   DVec<int32_t> srows, sitem0;         // super-long rows and their first item
   std::vector<int32_t> sptr_h;
   DVec<int32_t> ptr_d, iptr_d;         // device copies of ptr_h / iptr_h (persistent kernels)
-  DVec<uint32_t> cnt;                  // per super-long row: chunks finished (mod #chunks)
 };
 // lists over the row ranges `bounds` of a CSR with host row pointers rp
 void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<int32_t>& bounds, LongRows& L);
@@ -101,20 +100,6 @@ struct DColor {
   DVec<int32_t> heavy_nat;      // natural rows with more than kHeavyRow entries
   int32_t nheavy_nat = 0;
   LongRows blong;  // stored (colour) order, ranges per colour
-  // relaxation-coarsest sweep as a CUDA graph (relax_colored_graph), per
-  // (b, x, r) buffer set
-  struct SweepGraph {
-    cudaGraphExec_t exec = nullptr;
-    const void *b = nullptr, *x = nullptr, *r = nullptr;
-    long long launches = 0;
-  };
-  mutable SweepGraph sweep_graph;
-  DColor() = default;
-  DColor(const DColor&) = delete;
-  DColor& operator=(const DColor&) = delete;
-  ~DColor() {
-    if (sweep_graph.exec) cudaGraphExecDestroy(sweep_graph.exec);
-  }
 };
 constexpr int64_t kLongRow = 64;
 

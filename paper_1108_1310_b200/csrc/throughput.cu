@@ -246,8 +246,6 @@ void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<i
   up(L.sitem0, sitem0);
   up(L.ptr_d, L.ptr_h);
   up(L.iptr_d, L.iptr_h);
-  L.cnt.alloc(std::max<size_t>(srows.size(), 1), c.s);
-  L.cnt.zero();
   c.sync();
 }
 
@@ -486,7 +484,10 @@ __device__ __forceinline__ bool chunk_finish(const RelaxOp& o, int32_t it, doubl
   const int32_t j0 = o.sitem0[s], j1 = o.sitem0[s + 1];
   cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cnt(o.cnt[s]);
   const uint32_t old = cnt.fetch_add(1u, cuda::memory_order_acq_rel);
-  if ((old + 1) % (uint32_t)(j1 - j0) != 0) return false;
+  if (old + 1 != (uint32_t)(j1 - j0)) return false;
+  // the last chunk of the row: reset the counter for the next phase (nothing
+  // else touches it until a kernel boundary or grid barrier)
+  o.cnt[s] = 0u;
   double t = 0.0;
   for (int32_t j = j0; j < j1; ++j) t += __ldcg(o.ipart + j);
   *tot = t;
@@ -674,9 +675,23 @@ __global__ void __launch_bounds__(kRT) relax_coop_kernel(RelaxOp po, RelaxOp no,
 
 static RelaxOp relax_op(const int64_t* rp, const int32_t* col, const double* val, const double* diag,
                         const int32_t* row_ids, const int32_t* cptr, int32_t ncolors, const LongRows& L,
-                        double* ipart) {
+                        double* ipart, uint32_t* cnt) {
   return RelaxOp{rp, col, val, diag, row_ids, cptr, ncolors, L.rows.p, L.ptr_d.p, L.item_row.p, L.item_chunk.p,
-                 L.item_srow.p, L.iptr_d.p, L.sitem0.p, L.srows.p, L.sptr_h.back(), L.cnt.p, ipart, L.chunk};
+                 L.item_srow.p, L.iptr_d.p, L.sitem0.p, L.srows.p, L.sptr_h.back(), cnt, ipart, L.chunk};
+}
+
+// per-context scratch of the task kernels: chunk partials and row counters
+// (zeroed when allocated; every completed row resets its counter)
+static void relax_scratch(Ctx& c, int64_t nitems, int64_t nrows) {
+  if (c.ripart.n < std::max<int64_t>(nitems, 1)) {
+    c.ripart.alloc(std::max<int64_t>(nitems, 1), c.s);
+    ++c.rgen;
+  }
+  if (c.rcnt.n < std::max<int64_t>(nrows, 1)) {
+    c.rcnt.alloc(std::max<int64_t>(nrows, 1), c.s);
+    c.rcnt.zero();
+    ++c.rgen;
+  }
 }
 
 // One launch per colour (and per residual): a CTA per task, so the hardware
@@ -719,7 +734,8 @@ void residual_tasks(Ctx& c, const CSRv& a, const LongRows& nat, const double* b,
     cp.upload(ncp, 2);
     c.rtcptr_n = a.n;
   }
-  const RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, cp.p, 1, nat, ipart.p);
+  // a residual never finishes rows in place (residual_finish), so no counters
+  const RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, cp.p, 1, nat, ipart.p, nullptr);
   const std::vector<int32_t> nptr = {0, a.n};
   const int64_t T = phase_tasks_h(nptr, nat, 0, G);
   double* xm = const_cast<double*>(x);
@@ -736,17 +752,19 @@ void residual_tasks(Ctx& c, const CSRv& a, const LongRows& nat, const double* b,
 int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const double* b, double* x,
                         double* r) {
   const int G = cl.group == 8 ? 8 : 1;
+  relax_scratch(c, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back(), cl.blong.sptr_h.back());
   DVec<double>& ipart = c.ripart;
-  const int64_t nitems = std::max<int64_t>(1, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back());
-  if (ipart.n < nitems) ipart.alloc(nitems, c.s);
   DVec<int32_t>& nat_cptr = c.rcptr;
-  if (nat_cptr.n < 2) nat_cptr.alloc(2, c.s);
+  if (nat_cptr.n < 2) {
+    nat_cptr.alloc(2, c.s);
+    ++c.rgen;
+  }
   const int32_t ncp[2] = {0, a.n};
   nat_cptr.upload(ncp, 2);
   const RelaxOp po = relax_op(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p,
-                              (const int32_t*)(cl.rp.p + a.n + 1), cl.ncolors, cl.blong, ipart.p);
+                              (const int32_t*)(cl.rp.p + a.n + 1), cl.ncolors, cl.blong, ipart.p, c.rcnt.p);
   const RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, nat_cptr.p, 1, nat,
-                              ipart.p + cl.blong.iptr_h.back());
+                              ipart.p + cl.blong.iptr_h.back(), nullptr);
   const std::vector<int32_t> nptr = {0, a.n};
   double* nrm = c.dscal + 112;
   auto residual_norm = [&] {
@@ -780,8 +798,10 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
     fprintf(stderr, "[relax] r0 tasks %.6e exact %.6e |b| %.6e |x| %.6e n %d\n", r0, rx, nb, nx, a.n);
   }
   if (r0 == 0.0) return 0;
-  DColor::SweepGraph& g = cl.sweep_graph;
-  if (!g.exec || g.b != b || g.x != x || g.r != r) {
+  // the sweep graph is cached per context (its scratch pointers are the
+  // context's), keyed by the operator, the vectors and the scratch generation
+  Ctx::RelaxGraph& g = c.relax_graph;
+  if (!g.exec || g.key != &cl || g.b != b || g.x != x || g.r != r || g.gen != c.rgen) {
     if (g.exec) CK(cudaGraphExecDestroy(g.exec));
     g.exec = nullptr;
     const long long l0 = t_launches;
@@ -794,7 +814,7 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
     g.launches = t_launches - l0;
     g_launches -= g.launches;  // counted when the graph runs
     t_launches = l0;
-    g.b = b, g.x = x, g.r = r;
+    g.key = &cl, g.b = b, g.x = x, g.r = r, g.gen = c.rgen;
   }
   const double target = 1e-12 * r0;
   int sweeps = 0;
@@ -823,18 +843,20 @@ int relax_colored_coop(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& 
   if (const char* e = getenv("LAMG_RELAX_BLOCKS")) blocks = std::max(1, std::min(blocks, atoi(e)));
   DVec<double>& part = c.rpart;
   if (part.n < blocks) part.alloc(blocks, c.s);
+  relax_scratch(c, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back(), cl.blong.sptr_h.back());
   DVec<double>& ipart = c.ripart;
-  const int64_t nitems = std::max<int64_t>(1, (int64_t)cl.blong.iptr_h.back() + nat.iptr_h.back());
-  if (ipart.n < nitems) ipart.alloc(nitems, c.s);
   DVec<int32_t>& nat_cptr = c.rcptr;
-  if (nat_cptr.n < 2) nat_cptr.alloc(2, c.s);
+  if (nat_cptr.n < 2) {
+    nat_cptr.alloc(2, c.s);
+    ++c.rgen;
+  }
   const int32_t ncp[2] = {0, a.n};
   nat_cptr.upload(ncp, 2);
   int* sw = c.dflag + 30;
   RelaxOp po = relax_op(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, (const int32_t*)(cl.rp.p + a.n + 1),
-                        cl.ncolors, cl.blong, ipart.p);
+                        cl.ncolors, cl.blong, ipart.p, c.rcnt.p);
   RelaxOp no = relax_op(a.rp, a.col, a.val, a.diag, nullptr, nat_cptr.p, 1, nat,
-                        ipart.p + cl.blong.iptr_h.back());
+                        ipart.p + cl.blong.iptr_h.back(), nullptr);
   int32_t n = a.n;
   double* pp = part.p;
   // LAMG_RELAX_TIMING=1 (diagnostic): device timestamps of the first sweep's

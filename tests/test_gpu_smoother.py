@@ -158,3 +158,37 @@ def test_throughput_relaxation_coarsest(name, path, ctx, monkeypatch):
     want = Oracle("port").coarsest_relax(a, b, x0)
     dx, dw = x - x.mean(), want - want.mean()
     assert np.linalg.norm(dx - dw) <= 1e-7 * np.linalg.norm(dw)
+
+
+def test_concurrent_contexts_share_a_power_law_hierarchy():
+    """Two contexts (threads/streams) solving over one hierarchy at the same
+    time -- the relaxation's chunk counters and sweep graphs are per context,
+    so each solve equals the lone solve bit for bit."""
+    import threading
+
+    from paper_1108_1310_b200 import lamg as L
+    a = G.rmat(17, seed=5)
+    c0 = L.Context(0, L.MODE_THROUGHPUT)
+    h = L.setup(a, ctx=c0)
+    h.prepare_throughput()
+    assert h.levels[-1].coarsest == 2 and h.levels[-1].n > 40000
+    bs = [G.gaussian_rhs(a.n, 30 + j) for j in range(2)]
+    x0 = G.default_x0(a.n)
+    want = [L.solve(h, b, x0, ctx=c0)[0] for b in bs]
+    ctxs = [L.Context(0, L.MODE_THROUGHPUT) for _ in range(2)]
+    got = [[None] * 3 for _ in range(2)]
+
+    def run(j):
+        for rep in range(3):
+            got[j][rep] = L.solve(h, bs[j], x0, ctx=ctxs[j])[0]
+
+    th = [threading.Thread(target=run, args=(j,)) for j in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for j in range(2):
+        for rep in range(3):
+            assert np.array_equal(got[j][rep], want[j]), (j, rep)
+    for c in ctxs + [c0]:
+        c.close()
