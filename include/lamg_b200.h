@@ -229,7 +229,8 @@ int lamg_part_plan_sizes(const lamg_csr *a, const int32_t *bounds, int32_t npart
 int lamg_part_plan(const lamg_csr *a, const int32_t *bounds, int32_t nparts, int32_t part, int64_t *row_ptr,
                    int32_t *col, int32_t *ghost_gid, int32_t *recv_ptr, int32_t *send_ptr, int32_t *send_idx);
 /* device: a (host CSR, the whole level) is partitioned by bounds; this
- * process owns parts [first_part, first_part + nown) */
+ * process owns parts [first_part, first_part + nown). The communicator (if
+ * any) must outlive the partition. */
 int lamg_part_level_create(lamg_ctx *ctx, const lamg_csr *a, const int32_t *bounds, int32_t nparts,
                            int32_t first_part, int32_t nown, lamg_comm *comm, lamg_part_level **out);
 /* the finest level of a hierarchy, partitioned (bounds by lamg_part_bounds) */

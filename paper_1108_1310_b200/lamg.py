@@ -782,6 +782,7 @@ class PartLevel:
 
     def __init__(self, a, nparts: int, ctx: Context | None = None, bounds=None, comm: Comm | None = None):
         self.ctx = ctx or default_context()
+        self.comm = comm  # the library keeps a pointer: the communicator must outlive the partition
         self.n = a.n
         self.bounds = _i32(bounds if bounds is not None else part_bounds(a, nparts))
         arg = _CSRArg(a)
@@ -796,6 +797,7 @@ class PartLevel:
         """The finest level of `h` split into `nparts` row blocks (lamg_part_level_from_hier)."""
         self = cls.__new__(cls)
         self.ctx, self.n = h.ctx, h.n
+        self.comm, self.hier = comm, h  # both must outlive the partition
         self.p = C.c_void_p()
         first, nown = (0, nparts) if comm is None else (comm.rank, 1)
         _check(self.ctx.lib.lamg_part_level_from_hier(self.ctx.p, h.h, C.c_int32(nparts), C.c_int32(first),
