@@ -286,6 +286,13 @@ int lamg_ctx_set_mode(lamg_ctx* ctx, int mode) {
   });
 }
 
+int lamg_ctx_set_exact_levels(lamg_ctx* ctx, int32_t levels) {
+  return guarded([&] {
+    if (!ctx || levels < 0) throw LamgError(LAMG_E_ARGUMENT, "bad context or level count");
+    ctx->c.exact_levels = levels;
+  });
+}
+
 void lamg_ctx_destroy(lamg_ctx* ctx) {
   if (!ctx) return;
   Ctx& c = ctx->c;

@@ -193,6 +193,9 @@ struct Profile {
 struct Ctx {
   int device = 0;
   int mode = LAMG_MODE_VALIDATE;
+  // THROUGHPUT one-column solves sweep this many finest levels in the
+  // reference's exact order (the rest coloured); see lamg_ctx_set_exact_levels
+  int exact_levels = 1;
   int sms = 148;
   cudaStream_t s = nullptr;
   DevErr* derr = nullptr;       // device error slot

@@ -170,6 +170,14 @@ void build_schedule(Ctx& c, const CSRv& a, bool backward, Schedule& out) {
   int32_t w = 0;
   for (int32_t f = 0; f < nf; ++f) w = std::max(w, fp[f + 1] - fp[f]);
   out.max_width = w;
+  {
+    std::vector<int64_t> rph((size_t)n + 1);
+    CK(cudaMemcpyAsync(rph.data(), a.rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    int64_t ml = 0;
+    for (int32_t u = 0; u < n; ++u) ml = std::max(ml, rph[u + 1] - rph[u]);
+    out.max_len = ml;
+  }
   // heavy rows in sweep order, grouped by front
   DVec<uint8_t> hf(n, c.s);
   count_launch(), heavy_pos_kernel<<<blocks_for(n), kThreads, 0, c.s>>>(a, out.rows.p, n, hf.p);
@@ -260,9 +268,95 @@ __global__ void gs_fronts_kernel(CSRv a, const double* __restrict__ b, double* x
   }
 }
 
+// Exact-order sweep of a level whose rows all fit one 8-entry round (grids:
+// 7 entries), one column: each thread loads its row of the NEXT front (row
+// id, bounds, the 8 column/value pairs, b, diag) before the grid barrier, so
+// after it only the x gathers and the fold remain on the critical path.
+constexpr int kLightRow = 8;
+struct FrontRow {
+  int32_t u;
+  int32_t len;
+  double bu, d;
+  int32_t c[kLightRow];
+  double v[kLightRow];
+};
+__device__ __forceinline__ void front_row_load(const CSRv& a, const double* b, const int32_t* rows, int64_t i,
+                                               FrontRow& r) {
+  r.u = rows[i];
+  const int64_t k0 = a.rp[r.u];
+  r.len = (int32_t)(a.rp[r.u + 1] - k0);
+  r.bu = b ? b[r.u] : 0.0;
+  r.d = a.diag[r.u];
+#pragma unroll
+  for (int j = 0; j < kLightRow; ++j) {
+    const bool ok = j < r.len;
+    r.c[j] = ok ? a.col[k0 + j] : 0;
+    r.v[j] = ok ? a.val[k0 + j] : 0.0;
+  }
+}
+__global__ void gs_fronts_light_kernel(CSRv a, const double* __restrict__ b, double* x,
+                                       const int32_t* __restrict__ front_ptr, const int32_t* __restrict__ rows,
+                                       int32_t nfronts, int sweeps, int backward, DevErr* err) {
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  FrontRow pre;
+  bool have = false;
+  auto prefetch = [&](int32_t f) {
+    const int64_t i = front_ptr[f] + gtid;
+    have = i < front_ptr[f + 1];
+    if (have) front_row_load(a, b, rows, i, pre);
+  };
+  auto finish = [&](const FrontRow& r) {
+    double xv[kLightRow];
+#pragma unroll
+    for (int j = 0; j < kLightRow; ++j) xv[j] = j < r.len ? x[r.c[j]] : 0.0;
+    double s = r.bu;
+#pragma unroll
+    for (int j = 0; j < kLightRow; ++j)
+      if (j < r.len) s = s - r.v[j] * xv[j];
+    if (r.d == 0.0) {
+      if (r.len)
+        dev_report(err, backward ? (unsigned long long)(a.n - 1 - r.u) : (unsigned long long)r.u, DE_GS_SINGULAR,
+                   r.u, 0);
+      return;
+    }
+    x[r.u] = s / r.d;
+  };
+  if (nfronts > 0) prefetch(0);
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int32_t f = 0; f < nfronts; ++f) {
+      const int32_t fe = front_ptr[f + 1];
+      if (have) finish(pre);
+      for (int64_t i = front_ptr[f] + gtid + gstride; i < fe; i += gstride) {  // wide fronts
+        FrontRow r;
+        front_row_load(a, b, rows, i, r);
+        finish(r);
+      }
+      if (f + 1 < nfronts) prefetch(f + 1);
+      else if (sw + 1 < sweeps) prefetch(0);
+      grid_barrier();
+    }
+  }
+}
+
 void gs_exact(Ctx& c, const CSRv& a, const Schedule& sch, const double* b, double* x, int K,
               int sweeps, bool backward, bool check) {
   if (a.n == 0 || sweeps <= 0) return;
+  if (K == 1 && sch.max_len <= kLightRow && !getenv("LAMG_NO_LIGHT_FRONTS")) {
+    const int threads = 256;
+    int blocks = (int)std::min<int64_t>(c.max_coop_blocks((const void*)gs_fronts_light_kernel, threads),
+                                        std::max<int64_t>(1, ((int64_t)sch.max_width + threads - 1) / threads));
+    if (sch.max_width <= 2 * threads) blocks = 1;
+    CSRv av = a;
+    const int32_t* fp = sch.front_ptr.p;
+    const int32_t* rw = sch.rows.p;
+    int32_t nf = sch.nfronts;
+    int bw = backward ? 1 : 0;
+    void* args[] = {&av, (void*)&b, &x, (void*)&fp, (void*)&rw, &nf, &sweeps, &bw, &c.derr};
+    if (check) c.checked([&] { coop_launch(c, (const void*)gs_fronts_light_kernel, blocks, threads, args); });
+    else coop_launch(c, (const void*)gs_fronts_light_kernel, blocks, threads, args);
+    return;
+  }
   const int threads = 256;
   int64_t work = (int64_t)sch.max_width * K;
   int blocks = (int)std::min<int64_t>(c.max_coop_blocks((const void*)gs_fronts_kernel, threads),

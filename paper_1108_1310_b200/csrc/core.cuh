@@ -14,6 +14,7 @@ namespace lamgb {
 struct Schedule {
   int32_t nfronts = 0;
   int32_t max_width = 0;
+  int64_t max_len = 0;       // longest row (entries)
   DVec<int32_t> front_ptr;  // [nfronts+1]
   DVec<int32_t> rows;       // [n] rows, ascending within a front
   // heavy rows (hubs) are swept by a whole CTA: positions into `rows`,

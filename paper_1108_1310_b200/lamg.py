@@ -184,6 +184,10 @@ class Context:
         _check(self.lib.lamg_ctx_create(C.c_int(device), C.c_int(mode), C.byref(self.p)))
         self.mode = mode
 
+    def set_exact_levels(self, levels: int):
+        """THROUGHPUT one-column solves: finest levels swept in the reference's exact order."""
+        _check(self.lib.lamg_ctx_set_exact_levels(self.p, C.c_int32(levels)))
+
     def set_mode(self, mode: int):
         _check(self.lib.lamg_ctx_set_mode(self.p, C.c_int(mode)))
         self.mode = mode

@@ -193,6 +193,7 @@ def test_nccl_transport_single_rank():
     assert np.array_equal(pl.smooth(b, x, 2), want)
     pl.close()
     # the partitioned solve over the NCCL transport (allgathers by ncclBroadcast)
+    ctx.set_exact_levels(0)
     h = L.setup(a, ctx=ctx)
     bb, x0 = G.gaussian_rhs(a.n, 5), G.default_x0(a.n)
     x1, s1 = L.solve(h, bb, x0, ctx=ctx)
@@ -213,6 +214,7 @@ def test_partitioned_solve_bit_identical(name):
     from paper_1108_1310_b200 import lamg as L
     a = G.grid3d_7pt(48) if name == "grid3d_48" else G.make_config(2)
     ctx = L.Context(0, L.MODE_THROUGHPUT)
+    ctx.set_exact_levels(0)  # the partitioned finest level sweeps coloured
     h = L.setup(a, ctx=ctx)
     assert h.levels[1].kind == 2
     b, x0 = G.gaussian_rhs(a.n, 17), G.default_x0(a.n)
