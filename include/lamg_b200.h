@@ -125,10 +125,11 @@ typedef struct {
 /* ---- context ---------------------------------------------------------- */
 int lamg_ctx_create(int device, int mode, lamg_ctx **out);
 int lamg_ctx_set_mode(lamg_ctx *ctx, int mode);
-/* THROUGHPUT one-column solves: how many finest levels keep the reference's
- * exact Gauss-Seidel order (default 1; 0 = every level coloured). On config 2
- * the finest level's order decides the cycle count (exact: the reference's
- * 129, coloured: 141). Blocks of columns and partitioned solves sweep coloured. */
+/* THROUGHPUT one-column solves: how many of the finest SMOOTHING levels keep
+ * the reference's exact Gauss-Seidel order (default 1; 0 = every level
+ * coloured). The first smoothing level's order decides the cycle count
+ * (config 2: exact 129 = the reference's, coloured 141; RGG 2^20: 13 vs 15).
+ * Blocks of columns and partitioned solves sweep coloured. */
 int lamg_ctx_set_exact_levels(lamg_ctx *ctx, int32_t levels);
 void lamg_ctx_destroy(lamg_ctx *ctx);
 const char *lamg_last_error(void);

@@ -289,6 +289,11 @@ int lamg_ctx_set_mode(lamg_ctx* ctx, int mode) {
 int lamg_ctx_set_exact_levels(lamg_ctx* ctx, int32_t levels) {
   return guarded([&] {
     if (!ctx || levels < 0) throw LamgError(LAMG_E_ARGUMENT, "bad context or level count");
+    if (ctx->c.exact_levels != levels && ctx->c.ws) {
+      set_device(ctx->c);
+      ctx->c.sync();
+      ctx->c.ws->clear_graphs();  // captured cycles hold the previous smoother choice
+    }
     ctx->c.exact_levels = levels;
   });
 }

@@ -350,7 +350,18 @@ struct Driver {
   // reference's exact order: on config 2 the finest level's order alone moves
   // the cycle count from the reference's 129 to 141 coloured; exact on level 0
   // restores 129 for ~5% more time per solve (the light wavefront kernel)
-  int exact_levels() const { return c.exact_levels; }
+  // levels below first_smooth + c.exact_levels sweep exactly, where
+  // first_smooth is the finest level that smooths (level 0 on 3D grids; level
+  // 1 when the finest is eliminated, as on RGG and 2D grids)
+  int exact_levels() const {
+    int first = (int)h.levels.size();
+    for (size_t l = 0; l + 1 < h.levels.size(); ++l)
+      if (h.levels[l + 1]->kind == KIND_AGG) {
+        first = (int)l;
+        break;
+      }
+    return first + c.exact_levels;
+  }
   void gs(size_t l, const double* b, double* x, int sweeps) {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
