@@ -191,6 +191,8 @@ inline void set_mode(int mode) {
     case LAMG_E_INVALID_LAPLACIAN: throw InvalidLaplacianError(msg);
     case LAMG_E_DIMENSION_MISMATCH: throw DimensionMismatchError(msg);
     case LAMG_E_INCOMPATIBLE_RHS: throw IncompatibleRhsError(msg);
+    case LAMG_E_PARSE: throw ParseError(msg);
+    case LAMG_E_IO: throw IoError(msg);
     default: throw Error(msg);
   }
 }
@@ -466,6 +468,50 @@ inline SolveReport solve_prepared(const Prepared& p, std::span<const Real> b, st
   r.solve_work = work_edges / static_cast<double>(std::max<EntryCount>(p.a.m, 1));
   r.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return r;
+}
+
+// ------------------------------------------------------- Matrix Market files
+// matrix_market.hpp:14-52: read_matrix_market_file + assemble_problem in one
+// library call (multi-threaded parse, same CSR, warnings and errors)
+enum class MatrixKind { Auto, Adjacency, Laplacian };
+struct MatrixMarketOptions {
+  MatrixKind kind = MatrixKind::Auto;
+  bool absolute_weight_policy = true;
+};
+struct LoadedLaplacian {  // what assemble_problem(read_matrix_market_file(path)) yields
+  SparseLaplacian a;
+  bool was_laplacian = false;
+  std::vector<std::string> warnings;
+};
+
+inline LoadedLaplacian load_matrix_market_file(const std::string& path, const MatrixMarketOptions& opts = {}) {
+  lamg_mm* mm = nullptr;
+  const int kind = opts.kind == MatrixKind::Adjacency ? 1 : opts.kind == MatrixKind::Laplacian ? 2 : 0;
+  b200::check(lamg_mm_read(path.c_str(), kind, opts.absolute_weight_policy ? 1 : 0, &mm));
+  std::unique_ptr<lamg_mm, void (*)(lamg_mm*)> guard(mm, lamg_mm_destroy);
+  int32_t n = 0, lap = 0, nw = 0;
+  int64_t m = 0;
+  b200::check(lamg_mm_info(mm, &n, &m, &lap, &nw));
+  LoadedLaplacian out;
+  out.a.n = n;
+  out.a.m = m;
+  out.a.row_ptr.resize((std::size_t)n + 1);
+  out.a.col.resize((std::size_t)(2 * m));
+  out.a.val.resize((std::size_t)(2 * m));
+  out.a.diag.resize((std::size_t)n);
+  b200::check(lamg_mm_csr(mm, out.a.row_ptr.data(), out.a.col.data(), out.a.val.data(), out.a.diag.data()));
+  out.was_laplacian = lap != 0;
+  for (int32_t i = 0; i < nw; ++i) {
+    char buf[1024];
+    b200::check(lamg_mm_warning(mm, i, buf, (int32_t)sizeof buf));
+    out.warnings.emplace_back(buf);
+  }
+  return out;
+}
+
+inline void write_matrix_market_file(const std::string& path, const SparseLaplacian& a, bool as_laplacian = false) {
+  const lamg_csr v = b200::view(a);
+  b200::check(lamg_mm_write(path.c_str(), &v, as_laplacian ? 1 : 0));
 }
 
 }  // namespace lamg

@@ -56,5 +56,16 @@ int main() {
   lamg::Prepared p = lamg::prepare(d);
   lamg::SolveReport r = lamg::solve_prepared(p, std::vector<double>{1.0, 0.0, -1.0, 0.5, -0.25, -0.25, 0.0});
   std::printf("components %zu converged %d x6 %.1f\n", p.components.size(), (int)r.converged, r.x[6]);
+  // Matrix Market round trip (host only) and a parse error with the reference's text
+  const char* path = "/tmp/lamg_b200_facade_demo.mtx";
+  lamg::write_matrix_market_file(path, a);
+  lamg::LoadedLaplacian back = lamg::load_matrix_market_file(path);
+  std::printf("mm n %d m %lld same %d laplacian %d\n", back.a.n, (long long)back.a.m,
+              (int)(back.a.col == a.col && back.a.val == a.val && back.a.diag == a.diag), (int)back.was_laplacian);
+  try {
+    lamg::load_matrix_market_file("/nonexistent/x.mtx");
+  } catch (const lamg::IoError& e) {
+    std::printf("IoError: %s\n", e.what());
+  }
   return 0;
 }

@@ -35,3 +35,5 @@ def test_facade_runs_on_gpu(port):
     assert out[0].split()[3] == str(int(st["cycles"][0])), out[0]
     assert out[1].startswith("IncompatibleRhsError: right-hand side sum")
     assert out[2] == "components 3 converged 1 x6 0.0"
+    assert out[3] == f"mm n {a.n} m {a.m} same 1 laplacian 0", out[3]
+    assert out[4] == "IoError: cannot open: /nonexistent/x.mtx"
