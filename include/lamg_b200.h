@@ -246,7 +246,10 @@ void lamg_part_level_destroy(lamg_part_level *pl);
 /* lamg_solve with the finest level partitioned (THROUGHPUT, flat cycle, finest
  * level with an aggregation child): finest sweeps/residuals on the parts, the
  * residual allgathered, coarse levels replicated on every rank; bit-identical
- * to lamg_solve. b, x0, x: full host vectors (every rank passes all of b). */
+ * to lamg_solve on a context with lamg_ctx_set_exact_levels(ctx, 0) (the parts
+ * sweep coloured). pl must have been built on ctx (and, from a hierarchy, from
+ * h): LAMG_E_ARGUMENT otherwise. b, x0, x: full host vectors (every rank
+ * passes all of b). */
 int lamg_part_solve(lamg_ctx *ctx, const lamg_hier *h, lamg_part_level *pl, const double *b, const double *x0,
                     const lamg_cycle_cfg *cfg, double *x, lamg_solve_stats *stats, double *residuals,
                     int32_t cap);

@@ -369,7 +369,7 @@ int lamg_setup(lamg_ctx* ctx, const lamg_csr* a, int on_device, const lamg_setup
       delete h;
       throw;
     }
-    h->h->owner_stream = c.s;
+    h->h->mark_ready(c.s);
     *out = h;
   });
 }
@@ -440,7 +440,7 @@ int lamg_hier_download_op(const lamg_hier* h, int32_t l, int64_t* rp, int32_t* c
   return guarded([&] {
     const DLevel& L = level_of(h, l);
     CK(cudaSetDevice(h->h->device));
-    CK(cudaStreamSynchronize(h->h->owner_stream));
+    h->h->wait_ready();
     if (rp) CK(cudaMemcpy(rp, L.op.rp.p, sizeof(int64_t) * (L.op.n + 1), cudaMemcpyDeviceToHost));
     if (col) CK(cudaMemcpy(col, L.op.col.p, sizeof(int32_t) * 2 * L.op.m, cudaMemcpyDeviceToHost));
     if (val) CK(cudaMemcpy(val, L.op.val.p, sizeof(double) * 2 * L.op.m, cudaMemcpyDeviceToHost));
@@ -453,7 +453,7 @@ int lamg_hier_download_agg(const lamg_hier* h, int32_t l, int32_t* aggregate_of,
     const DLevel& L = level_of(h, l);
     if (!L.agg) throw LamgError(LAMG_E_ARGUMENT, "level is not an aggregation level");
     CK(cudaSetDevice(h->h->device));
-    CK(cudaStreamSynchronize(h->h->owner_stream));
+    h->h->wait_ready();
     if (aggregate_of)
       CK(cudaMemcpy(aggregate_of, L.agg->aggregate_of.p, sizeof(int32_t) * L.agg->fine_n, cudaMemcpyDeviceToHost));
     if (seed_of) CK(cudaMemcpy(seed_of, L.agg->seed_of.p, sizeof(int32_t) * L.agg->coarse_n, cudaMemcpyDeviceToHost));
@@ -480,7 +480,7 @@ int lamg_hier_download_stage(const lamg_hier* h, int32_t l, int32_t s, int32_t* 
     if (s < 0 || s >= (int32_t)L.stages.size()) throw LamgError(LAMG_E_ARGUMENT, "stage out of range");
     const DStage& st = *L.stages[s];
     CK(cudaSetDevice(h->h->device));
-    CK(cudaStreamSynchronize(h->h->owner_stream));
+    h->h->wait_ready();
     auto cp = [](void* dst, const void* src, size_t bytes) {
       if (dst && bytes) CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
     };
@@ -1022,6 +1022,9 @@ int lamg_k_coarsest_relax(lamg_ctx* ctx, const lamg_csr* a, const double* b, dou
     relax_solve(c, av, sch, col.get(), exact ? nullptr : &nat, db.p, dx.p, r, &sw, exact);
     dx.download(x, a->n);
     c.sync();
+    // the cached sweep graph points at this call's temporaries
+    if (c.relax_graph.exec) CK(cudaGraphExecDestroy(c.relax_graph.exec));
+    c.relax_graph.exec = nullptr;
   });
 }
 
@@ -1070,6 +1073,7 @@ struct lamg_part_level {
   lamg_ctx* ctx;
   std::unique_ptr<PartLevel> pl;
   int32_t n;
+  uint64_t hier_uid = 0;  // DHier::uid of the hierarchy whose finest level this is (0: built from a CSR)
 };
 
 int lamg_comm_unique_id(char id[128]) {
@@ -1184,6 +1188,7 @@ int lamg_part_level_from_hier(lamg_ctx* ctx, const lamg_hier* hier, int32_t npar
     auto* h = new lamg_part_level();
     h->ctx = ctx;
     h->n = op.n;
+    h->hier_uid = hier->h->uid;
     try {
       h->pl = std::make_unique<PartLevel>(c, op.view(), rp, col, val, diag, b, first_part, nown,
                                           comm ? comm->c.get() : nullptr);
@@ -1198,6 +1203,11 @@ int lamg_part_level_from_hier(lamg_ctx* ctx, const lamg_hier* hier, int32_t npar
 int lamg_part_solve(lamg_ctx* ctx, const lamg_hier* h, lamg_part_level* pl, const double* b, const double* x0,
                     const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals, int32_t cap) {
   if (!pl) return guarded([] { throw LamgError(LAMG_E_ARGUMENT, "null partition"); });
+  // the parts enqueue on their own context's stream, the coarse levels on ctx's
+  if (pl->ctx != ctx)
+    return guarded([] { throw LamgError(LAMG_E_ARGUMENT, "partition was built on another context"); });
+  if (h && h->h && pl->hier_uid && pl->hier_uid != h->h->uid)
+    return guarded([] { throw LamgError(LAMG_E_ARGUMENT, "partition was built from another hierarchy"); });
   return solve_common(ctx, h, b, x0, false, cfg, x, stats, residuals, cap, pl->pl.get());
 }
 

@@ -219,8 +219,8 @@ struct Ctx {
   DVec<uint32_t> rcnt;          // chunk counters of super-long rows (return to 0 after each row)
   int64_t rgen = 0;
   struct RelaxGraph {
-    const void* key = nullptr;  // the DColor
-    const void *b = nullptr, *x = nullptr, *r = nullptr;
+    uint64_t key = 0;  // DColor::uid (monotonic: never reused, unlike an address)
+    const void *op = nullptr, *b = nullptr, *x = nullptr, *r = nullptr;  // natural operator values, vectors
     int64_t gen = -1;
     cudaGraphExec_t exec = nullptr;
     long long launches = 0;

@@ -84,7 +84,13 @@ void build_long_rows(Ctx& c, const std::vector<int64_t>& rp, const std::vector<i
 // colouring) and a copy of the operator whose rows are stored colour by
 // colour. A coloured sweep is a sequential sweep in colour-permuted order:
 // same hierarchy, different smoother.
+inline uint64_t next_object_uid() {
+  static std::atomic<uint64_t> c{1};
+  return c++;
+}
+
 struct DColor {
+  uint64_t uid = next_object_uid();  // keys cached sweep graphs (addresses get reused)
   int32_t ncolors = 0;
   int group = 1;                // lanes per row in the throughput kernels (1, 4 or 8)
   std::vector<int32_t> cptr_h;  // [ncolors+1] row ranges of each colour
@@ -127,7 +133,19 @@ struct DHier {
   uint64_t seed = 0;
   std::vector<std::string> warnings;
   int device = 0;
-  cudaStream_t owner_stream = nullptr;
+  // recorded on the setup context's stream when setup returns: host reads of
+  // the hierarchy wait on it (the event outlives the context and its stream)
+  cudaEvent_t ready = nullptr;
+  void mark_ready(cudaStream_t s) {
+    if (!ready) CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, s));
+  }
+  void wait_ready() const {
+    if (ready) CK(cudaEventSynchronize(ready));
+  }
+  ~DHier() {
+    if (ready) cudaEventDestroy(ready);
+  }
   // throughput mode (colour-permuted copies), built on demand
   std::atomic<bool> throughput_ready{false};
   std::mutex prep_mu;  // concurrent solves on one hierarchy (one context each) build it once
@@ -140,11 +158,7 @@ struct DHier {
     build();
     throughput_ready.store(true, std::memory_order_release);
   }
-  uint64_t uid = next_uid();  // workspaces key on this, not on the address
-  static uint64_t next_uid() {
-    static std::atomic<uint64_t> c{1};
-    return c++;
-  }
+  uint64_t uid = next_object_uid();  // workspaces key on this, not on the address
 };
 
 // assemble_canonical (sparse_laplacian.cpp:60-104) of a sorted, merged u<v

@@ -396,11 +396,12 @@ struct Driver {
     LevelWS& w = ws.lv[l];
     LevelWS& wc = ws.lv[l + 1];
     const bool adaptive = cfg.correction == 1;
+    static const bool trace = getenv("LAMG_TRACE") != nullptr;
     int nsaved = 0;
     for (int i = 0; i < theta; ++i) {
       if (child.nu_pre) gs(l, b, x, child.nu_pre);
       resid(l, b, x, w.r.p);
-      if (getenv("LAMG_TRACE") && K == 1)
+      if (trace && K == 1)
         fprintf(stderr, "[trace]   l=%zu pre-smoothed |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
       if (adaptive) {
         if (nsaved >= 2) throw LamgError(LAMG_E_ERROR, "recombination supports at most two saved iterates");
@@ -418,12 +419,12 @@ struct Driver {
       visit(l + 1, wc.b.p, wc.x.p, theta_child);
       if (K > 1) binterpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x, K);
       else interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
-      if (getenv("LAMG_TRACE") && K == 1) {
+      if (trace && K == 1) {
         resid(l, b, x, w.r.p);
         fprintf(stderr, "[trace]   l=%zu corrected |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
       }
       if (child.nu_post) gs(l, b, x, child.nu_post);
-      if (getenv("LAMG_TRACE") && K == 1) {
+      if (trace && K == 1) {
         resid(l, b, x, w.r.p);
         fprintf(stderr, "[trace]   l=%zu post-smoothed |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
       }
@@ -500,6 +501,14 @@ static bool prepare_solve(Ctx& c, const DHier& h, const CycleCfg& cfg, bool exac
   return use_tail;
 }
 
+// a captured cycle depends on the credits at its start and on mu (baked
+// into the restriction and tail kernel arguments)
+static std::vector<double> graph_key(const std::vector<double>& credits, const CycleCfg& cfg) {
+  std::vector<double> k = credits;
+  k.push_back(cfg.mu);
+  return k;
+}
+
 // cycle.cpp:221-273; b, x0, x are device pointers of the finest size
 int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, const CycleCfg& cfg,
                  double* x, SolveResult& res) {
@@ -550,12 +559,14 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
       fold_norm2(c, exact, ws.lv[0].r.p, n, rn_d);
     };
     if (use_graphs) {
+      // the captured kernels bake in the credits and CycleConfig::mu
+      const std::vector<double> key = graph_key(d.credits.credit, cfg);
       Workspace::CycleGraph* g = nullptr;
       for (auto& e : ws.graphs)
-        if (e.key == d.credits.credit) g = &e;
+        if (e.key == key) g = &e;
       if (!g) {
         Workspace::CycleGraph e;
-        e.key = d.credits.credit;
+        e.key = key;
         const double wc = c.work;
         const long long l0 = t_launches;
         cudaGraph_t graph;
@@ -614,7 +625,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
 // mode). The visit sequence is data-independent (LevelCredit), so one cycle
 // schedule -- one CUDA graph per credit state -- serves every column; each
 // column is copied out at the cycle where its own test (r <= r0/1e10, or
-// divergence) fires, exactly the iterate a one-column solve returns.
+// divergence) fires. A column's bits do not depend on the batch it rides in.
 int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const double* X0, const CycleCfg& cfg,
                        double* X, std::vector<SolveResult>& res) {
   if (nrhs < 1 || nrhs > 32) throw LamgError(LAMG_E_ARGUMENT, "batched solve takes 1..32 right-hand sides");
@@ -703,12 +714,14 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
       bcolsum(c, Rw, n, K, true, rn_d);
     };
     if (use_graphs) {
+      // the captured kernels bake in the credits and CycleConfig::mu
+      const std::vector<double> key = graph_key(d.credits.credit, cfg);
       Workspace::CycleGraph* g = nullptr;
       for (auto& e : ws.graphs)
-        if (e.key == d.credits.credit) g = &e;
+        if (e.key == key) g = &e;
       if (!g) {
         Workspace::CycleGraph e;
-        e.key = d.credits.credit;
+        e.key = key;
         const double wc = c.work;
         const long long l0 = t_launches;
         cudaGraph_t graph;

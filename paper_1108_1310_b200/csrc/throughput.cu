@@ -799,9 +799,10 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
   }
   if (r0 == 0.0) return 0;
   // the sweep graph is cached per context (its scratch pointers are the
-  // context's), keyed by the operator, the vectors and the scratch generation
+  // context's), keyed by the colouring's uid, the natural operator, the
+  // vectors and the scratch generation
   Ctx::RelaxGraph& g = c.relax_graph;
-  if (!g.exec || g.key != &cl || g.b != b || g.x != x || g.r != r || g.gen != c.rgen) {
+  if (!g.exec || g.key != cl.uid || g.op != a.val || g.b != b || g.x != x || g.r != r || g.gen != c.rgen) {
     if (g.exec) CK(cudaGraphExecDestroy(g.exec));
     g.exec = nullptr;
     const long long l0 = t_launches;
@@ -814,7 +815,7 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
     g.launches = t_launches - l0;
     g_launches -= g.launches;  // counted when the graph runs
     t_launches = l0;
-    g.key = &cl, g.b = b, g.x = x, g.r = r, g.gen = c.rgen;
+    g.key = cl.uid, g.op = a.val, g.b = b, g.x = x, g.r = r, g.gen = c.rgen;
   }
   const double target = 1e-12 * r0;
   int sweeps = 0;
