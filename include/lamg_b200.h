@@ -215,6 +215,12 @@ int lamg_hier_color_count(const lamg_hier *h, int32_t level, int32_t *ncolors);
 int lamg_hier_download_colors(const lamg_hier *h, int32_t level, int32_t *row_ids, int32_t *color_ptr);
 int lamg_hier_smooth(lamg_ctx *ctx, const lamg_hier *h, int32_t level, int32_t nrhs, const double *b,
                      double *x, int32_t sweeps);
+/* the same in the reference's exact row order (gauss_seidel_sweep,
+ * smoothing.cpp:29-40, per column): nrhs == 1 the wavefront kernel; nrhs in
+ * {4,8,16,32} the ticketed K-column sweep the THROUGHPUT block solve uses on
+ * its exact levels. Bit-identical per column to the reference sweep. */
+int lamg_hier_smooth_exact(lamg_ctx *ctx, const lamg_hier *h, int32_t level, int32_t nrhs, const double *b,
+                           double *x, int32_t sweeps);
 
 /* ---- fine-level node-block partition with halo exchange (SURVEY 8(e)
  * mode 2). A level operator split into `nparts` contiguous row blocks

@@ -4,6 +4,7 @@
 // in every lane: one transaction), the x gathers of the K columns are one
 // coalesced K*8-byte segment, and lane k folds its column in entry order.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "batch.cuh"
@@ -16,25 +17,6 @@ constexpr int kBT = 256;  // threads per block of the batched kernels
 
 inline int bblocks(int64_t threads) { return (int)std::max<int64_t>(1, (threads + kBT - 1) / kBT); }
 
-// V = 4 columns per thread (two 16-byte loads per gather), K/V threads per
-// row: the row's entries are loaded once per K/V threads instead of once per
-// lane, so the instruction count per row drops ~V-fold; each column is still
-// folded in entry order (same arithmetic as one thread per column).
-constexpr int kV = 4;
-// a thread's four columns of one node-major row: ONE 256-bit access on
-// sm_100 (LDG.E.ENL2.256 / STG.E.ENL2.256) instead of two 128-bit ones --
-// half the L1TEX requests of the gathers, which the block sweep is bound by
-struct d4 {
-  double x, y, z, w;
-};
-__device__ __forceinline__ d4 ld4(const double* p) {
-  d4 r;
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
-}
 template <int K, bool SUB>
 __device__ __forceinline__ void fold4(double (&s)[kV], const int32_t* __restrict__ col,
                                       const double* __restrict__ val, const double* X, int64_t b, int64_t e, int k0) {
@@ -103,6 +85,120 @@ __global__ void __launch_bounds__(kBT, MINB) bgs_kernel(const int64_t* __restric
   }
 }
 
+// ---------------------------------------------- exact-order block sweep
+// gauss_seidel_sweep (smoothing.cpp:29-40) in the reference's row order for
+// K columns at once, without a grid barrier: the level's wavefronts (rows
+// whose lower neighbours all lie in earlier fronts) are cut into items of at
+// most kExactItemRows rows (ExactItems). A persistent grid claims items by a
+// ticket in front order; an item of front g waits (ld.acquire) until every
+// item of front g-1 has released its done counter, so front g-1 complete
+// implies every earlier front complete, and every row reads exactly the
+// values the sequential sweep reads. Tickets are handed out in order and an
+// item only waits on smaller tickets held by running CTAs: no co-residency
+// requirement, so concurrent lanes share the SMs. Each column's fold is
+// s = b; s -= a_uv x_v in the row's column order; x_u = s / d_u --
+// bit-identical per column to the one-column exact sweep.
+__device__ __forceinline__ int ld_acquire_i32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// One item per CTA pass: kExactItemRows rows x K/4 threads per row. Before
+// waiting on front g-1 the CTA loads everything that does not depend on it:
+// the rows, their extents, the first kXU entries (columns and values), b, the
+// diagonal and -- once the previous sweep is complete -- x of the upper
+// neighbours (col > u: rows of later fronts, not written before this item).
+// After the acquire only the lower neighbours' x (just written, L2 hits) are
+// gathered, then the fold in column order and the store.
+constexpr int kXU = 8;
+template <int K, bool PRE>
+__global__ void __launch_bounds__(kBT, PRE ? 2 : 3) bgs_exact_kernel(
+    CSRv a, const int32_t* __restrict__ rows, const int32_t* __restrict__ item_front,
+    const int32_t* __restrict__ item_r0, const int32_t* __restrict__ item_r1, const int32_t* __restrict__ front_items,
+    int32_t nfronts, int32_t nitems, int sweeps, const double* __restrict__ B, double* X, int32_t* ctl) {
+  constexpr int T = K / kV;  // threads per row
+  __shared__ int32_t s_t, s_up;
+  int32_t* done = ctl + 1;  // [sweeps * nfronts]
+  const int32_t total = nitems * sweeps;
+  const int k0 = (int)(threadIdx.x % T) * kV;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int32_t t = atomicAdd(ctl, 1);
+      s_t = t;
+      int up = 1;  // upper neighbours hold their final previous-sweep values
+      if (PRE && t < total) {
+        const int32_t sw = t / nitems;
+        if (sw > 0) up = ld_acquire_i32(done + sw * nfronts - 1) >= __ldg(front_items + nfronts - 1);
+      }
+      s_up = up;
+    }
+    __syncthreads();
+    const int32_t t = s_t;
+    if (t >= total) break;
+    const int32_t sw = t / nitems, it = t - sw * nitems;
+    const int32_t f = __ldg(item_front + it);
+    const int32_t g = sw * nfronts + f;
+    const int32_t r0 = __ldg(item_r0 + it), r1 = __ldg(item_r1 + it);
+    const int32_t i = r0 + (int32_t)(threadIdx.x / T);
+    const bool act = i < r1;
+    int32_t u = 0;
+    int64_t e0 = 0, e1 = 0;
+    double d = 1.0;
+    d4 bv{0.0, 0.0, 0.0, 0.0};
+    int32_t c[kXU];
+    double v[kXU];
+    d4 xv[kXU];
+    if (act) {
+      u = __ldg(rows + i);
+      e0 = __ldg(a.rp + u);
+      e1 = __ldg(a.rp + u + 1);
+      d = __ldg(a.diag + u);
+      bv = ld4(B + (int64_t)u * K + k0);
+    }
+#pragma unroll
+    for (int j = 0; j < kXU; ++j) {
+      const bool ok = e0 + j < e1;
+      c[j] = ok ? __ldg(a.col + e0 + j) : 0;
+      v[j] = ok ? __ldg(a.val + e0 + j) : 0.0;
+    }
+    const bool up = PRE && s_up;
+#pragma unroll
+    for (int j = 0; j < kXU; ++j)
+      xv[j] = (up && e0 + j < e1 && c[j] > u) ? ld4_cg(X + (int64_t)c[j] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x == 0 && g > 0) {
+      const int32_t need = __ldg(front_items + (g - 1) % nfronts);
+      while (ld_acquire_i32(done + g - 1) < need) __nanosleep(20);
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < kXU; ++j)
+        if (e0 + j < e1 && !(up && c[j] > u)) xv[j] = ld4_cg(X + (int64_t)c[j] * K + k0);
+      double s0 = bv.x, s1 = bv.y, s2 = bv.z, s3 = bv.w;
+#pragma unroll
+      for (int j = 0; j < kXU; ++j)
+        if (e0 + j < e1) {
+          s0 = s0 - v[j] * xv[j].x;
+          s1 = s1 - v[j] * xv[j].y;
+          s2 = s2 - v[j] * xv[j].z;
+          s3 = s3 - v[j] * xv[j].w;
+        }
+      for (int64_t e = e0 + kXU; e < e1; ++e) {  // long rows: the rest in column order
+        const d4 q = ld4_cg(X + (int64_t)__ldg(a.col + e) * K + k0);
+        const double w = __ldg(a.val + e);
+        s0 = s0 - w * q.x;
+        s1 = s1 - w * q.y;
+        s2 = s2 - w * q.z;
+        s3 = s3 - w * q.w;
+      }
+      if (d != 0.0) st4(X + (int64_t)u * K + k0, s0 / d, s1 / d, s2 / d, s3 / d);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(done + g, 1);
+  }
+}
+
 // Long rows (more than kLongRow entries): one CTA per row -- or per chunk of
 // L.chunk entries for the longest -- folds 32 strided slices of the entries
 // for all K columns; slice partials combine in slice order, chunk sums in
@@ -143,7 +239,7 @@ __device__ __forceinline__ void fold4_strided(double (&s)[kV], const int32_t* __
 template <int K>
 __device__ __forceinline__ double long_chunk_dot(const int32_t* __restrict__ col, const double* __restrict__ val,
                                                  const double* X, int64_t cb, int64_t ce) {
-  __shared__ double sh[kSL * 32];
+  __shared__ double sh[kSL * K];
   constexpr int Q = K / kV;
   for (int pr = threadIdx.x; pr < kSL * Q; pr += blockDim.x) {
     const int sl = pr / Q, k0 = (pr % Q) * kV;
@@ -284,7 +380,7 @@ __global__ void bcoarsen_kernel(StageV s, const double* __restrict__ B, double* 
 template <int K>
 __global__ void __launch_bounds__(kBT) bcoarsen_long_kernel(StageV s, const double* __restrict__ B,
                                                             double* __restrict__ Bc) {
-  __shared__ double sh[kSL * 32];
+  __shared__ double sh[kSL * K];
   const int32_t q = s.tlong[blockIdx.x];
   const int64_t j0 = s.t_ptr[q], j1 = s.t_ptr[q + 1];
   for (int pr = threadIdx.x; pr < kSL * K; pr += blockDim.x) {
@@ -422,7 +518,9 @@ void dispatch_k(int K, F&& f) {
     case 8: f(std::integral_constant<int, 8>{}); break;
     case 16: f(std::integral_constant<int, 16>{}); break;
     case 32: f(std::integral_constant<int, 32>{}); break;
-    default: throw LamgError(LAMG_E_ARGUMENT, "batch width must be 4, 8, 16 or 32");
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    default: throw LamgError(LAMG_E_ARGUMENT, "batch width must be 4, 8, 16, 32, 64 or 128");
   }
 }
 
@@ -462,6 +560,38 @@ void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X
       }
   });
   CK_LAUNCH();
+}
+
+void bgs_exact(Ctx& c, const CSRv& a, const Schedule& sch, const ExactItems& it, const double* B, double* X,
+               int sweeps, int K, int32_t* ctl) {
+  if (a.n == 0 || sweeps <= 0 || it.nitems == 0) return;
+  if (it.rows * std::max(1, K / kV) > kBT) throw LamgError(LAMG_E_ERROR, "exact sweep items too large for the block width");
+  static const int env_ctas = [] {
+    const char* e = getenv("LAMG_XB_CTAS");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  static const bool pre = [] {
+    const char* e = getenv("LAMG_XB_PRE");
+    return !(e && atoi(e) == 0);
+  }();
+  for (int s0 = 0; s0 < sweeps; s0 += kMaxExactSweeps) {
+    const int ns = std::min(kMaxExactSweeps, sweeps - s0);
+    const int64_t total = (int64_t)it.nitems * ns;
+    // a persistent grid of two CTAs per SM: an average cfg2 front (5.5k rows,
+    // ~170 items) in one pass
+    const int ctas = (int)std::min<int64_t>(total, env_ctas ? env_ctas : 2 * c.sms);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(int32_t) * (1 + (size_t)ns * it.nfronts), c.s));
+    dispatch_k(K, [&](auto kc) {
+      constexpr int KK = decltype(kc)::value;
+      if (pre)
+        count_launch(), bgs_exact_kernel<KK, true><<<ctas, kBT, 0, c.s>>>(
+            a, sch.rows.p, it.front.p, it.r0.p, it.r1.p, it.count.p, it.nfronts, it.nitems, ns, B, X, ctl);
+      else
+        count_launch(), bgs_exact_kernel<KK, false><<<ctas, kBT, 0, c.s>>>(
+            a, sch.rows.p, it.front.p, it.r0.p, it.r1.p, it.count.p, it.nfronts, it.nitems, ns, B, X, ctl);
+    });
+    CK_LAUNCH();
+  }
 }
 
 void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const double* X, double* R, int K) {
@@ -585,8 +715,8 @@ void brelax(Ctx& c, const CSRv& a, const DColor& cl, const LongRows& nat, const 
             int K, std::vector<int>& sweeps) {
   sweeps.assign(K, 0);
   int32_t* done = c.dbdone;
-  double* nrm = c.dbscal;          // [K]
-  double* sums = c.dbscal + 64;    // [K]
+  double* nrm = c.dbscal;                  // [K]
+  double* sums = c.dbscal + kMaxBlock;     // [K]
   std::vector<double> r0(K), rn(K);
   std::vector<int32_t> hdone(K, 0);
   bresidual(c, a, nat, B, X, R, K);

@@ -163,7 +163,7 @@ void fill_stats(const SolveResult& res, lamg_solve_stats* stats, double* residua
     for (int32_t i = 0; i < cap && i < (int32_t)res.residuals.size(); ++i) residuals[i] = res.residuals[i];
 }
 
-// nrhs right-hand sides, RHS-major [nrhs][n]: blocks of <= 32 columns in
+// nrhs right-hand sides, RHS-major [nrhs][n]: blocks of <= kMaxBlock columns in
 // THROUGHPUT mode (batch.cuh), one reference-order solve per column otherwise
 int solve_batch_common(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const double* b, const double* x0, bool dev,
                        const lamg_cycle_cfg* cfg, double* x, lamg_solve_stats* stats, double* residuals,
@@ -185,7 +185,7 @@ int solve_batch_common(lamg_ctx* ctx, const lamg_hier* h, int32_t nrhs, const do
       cc.divergence_factor = cfg->divergence_factor;
     }
     const bool blocked = c.mode == LAMG_MODE_THROUGHPUT && cc.correction == 0 && nrhs > 1;
-    const int chunk = blocked ? 32 : 1;
+    const int chunk = blocked ? kMaxBlock : 1;
     DVec<double> db, dx0, dx;
     if (!dev) {
       const int64_t w = std::min<int64_t>(nrhs, chunk) * n;
@@ -267,13 +267,13 @@ int lamg_ctx_create(int device, int mode, lamg_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
     CK(cudaMalloc(&c.derr, sizeof(DevErr)));
     CK(cudaMallocHost(&c.herr, sizeof(DevErr)));
-    CK(cudaMallocHost(&c.hscal, 64 * sizeof(double)));
+    CK(cudaMallocHost(&c.hscal, 4 * kMaxBlock * sizeof(double)));
     CK(cudaMalloc(&c.dflag, 64 * sizeof(int)));
     CK(cudaMalloc(&c.dscal, 256 * sizeof(double)));
     CK(cudaMalloc(&c.dpart, 256 * sizeof(double)));
-    CK(cudaMalloc(&c.dbpart, (size_t)32 * kColChunks * sizeof(double)));
-    CK(cudaMalloc(&c.dbscal, 256 * sizeof(double)));
-    CK(cudaMalloc(&c.dbdone, 64 * sizeof(int32_t)));
+    CK(cudaMalloc(&c.dbpart, (size_t)kMaxBlock * kColChunks * sizeof(double)));
+    CK(cudaMalloc(&c.dbscal, 8 * kMaxBlock * sizeof(double)));
+    CK(cudaMalloc(&c.dbdone, kMaxBlock * sizeof(int32_t)));
     c.clear_err();
     *out = x;
   });
@@ -289,10 +289,12 @@ int lamg_ctx_set_mode(lamg_ctx* ctx, int mode) {
 int lamg_ctx_set_exact_levels(lamg_ctx* ctx, int32_t levels) {
   return guarded([&] {
     if (!ctx || levels < 0) throw LamgError(LAMG_E_ARGUMENT, "bad context or level count");
-    if (ctx->c.exact_levels != levels && ctx->c.ws) {
+    if (ctx->c.exact_levels != levels && (ctx->c.ws || ctx->c.bws)) {
       set_device(ctx->c);
       ctx->c.sync();
-      ctx->c.ws->clear_graphs();  // captured cycles hold the previous smoother choice
+      // captured cycles hold the previous smoother choice
+      if (ctx->c.ws) ctx->c.ws->clear_graphs();
+      if (ctx->c.bws) ctx->c.bws->clear_graphs();
     }
     ctx->c.exact_levels = levels;
   });
@@ -665,20 +667,47 @@ int lamg_hier_smooth(lamg_ctx* ctx, const lamg_hier* h, int32_t l, int32_t nrhs,
   });
 }
 
+int lamg_hier_smooth_exact(lamg_ctx* ctx, const lamg_hier* h, int32_t l, int32_t nrhs, const double* b, double* x,
+                           int32_t sweeps) {
+  return guarded([&] {
+    if (!ctx || !h || !h->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
+    Ctx& c = ctx->c;
+    set_device(c);
+    const DLevel& L = level_of(h, l);
+    const int64_t len = (int64_t)L.op.n * nrhs;
+    DVec<double> db(len, c.s), dx(len, c.s);
+    db.upload(b, len);
+    dx.upload(x, len);
+    if (nrhs == 1) {
+      gs_exact(c, L.op.view(), L.sched, db.p, dx.p, 1, sweeps);
+    } else {
+      if (!batch_width_ok(nrhs)) throw LamgError(LAMG_E_ARGUMENT, "batch width must be 4, 8, 16, 32, 64 or 128");
+      ExactItems it;
+      build_exact_items(c, L.sched, 32 >> exact_table_for(nrhs), it);
+      DVec<int32_t> ctl(1 + (int64_t)kMaxExactSweeps * std::max(1, it.nfronts), c.s);
+      bgs_exact(c, L.op.view(), L.sched, it, db.p, dx.p, sweeps, nrhs, ctl.p);
+    }
+    dx.download(x, len);
+    c.sync();
+  });
+}
+
 // -------------------------------------------------------------- profiling
 int lamg_ctx_profile(lamg_ctx* ctx, int enable) {
   return guarded([&] {
     Ctx& c = ctx->c;
     c.prof.enabled = enable != 0;
-    c.prof.used[0] = c.prof.used[1] = 0;
-    c.prof.bytes[0] = c.prof.bytes[1] = 0.0;
+    for (int k = 0; k < kProfClasses; ++k) {
+      c.prof.used[k] = 0;
+      c.prof.bytes[k] = 0.0;
+    }
   });
 }
 
 int lamg_ctx_profile_read(lamg_ctx* ctx, int kernel, int64_t* launches, double* total_ms, double* bytes) {
   return guarded([&] {
     Ctx& c = ctx->c;
-    if (kernel < 0 || kernel > 1) throw LamgError(LAMG_E_ARGUMENT, "kernel class 0 (gs) or 1 (residual)");
+    if (kernel < 0 || kernel >= kProfClasses) throw LamgError(LAMG_E_ARGUMENT, "bad profile class");
     c.sync();
     double tot = 0.0;
     for (int64_t i = 0; i < c.prof.used[kernel]; ++i) {

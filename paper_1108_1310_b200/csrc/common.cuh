@@ -183,11 +183,17 @@ struct DCSR {  // owning device CSR
 // ---------------------------------------------------------------- context
 struct Workspace;  // solve.cuh
 
+// lamg_ctx_profile: CUDA events around kernel groups of a solve (graphs off).
+// Class 0 / 1: the finest level's Gauss-Seidel / residual launches (the
+// bench's roofline kernels); class 2 + 4 l + {0,1,2,3}: level l's sweeps,
+// residuals, transfers (restriction, interpolation, elimination stages) and
+// on-device tail visits rooted at l (a per-level time breakdown).
+constexpr int kProfClasses = 2 + 4 * 64;
 struct Profile {
   bool enabled = false;
-  std::vector<cudaEvent_t> ev[2];  // start/stop pairs per kernel class
-  int64_t used[2] = {0, 0};
-  double bytes[2] = {0, 0};
+  std::vector<cudaEvent_t> ev[kProfClasses];  // start/stop pairs per kernel class
+  int64_t used[kProfClasses] = {};
+  double bytes[kProfClasses] = {};
 };
 
 struct Ctx {

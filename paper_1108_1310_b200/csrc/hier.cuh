@@ -111,6 +111,23 @@ constexpr int64_t kLongRow = 64;
 
 constexpr int64_t kHeavyRow = 2048;
 
+// Exact-order sweep of a K-column block without a grid barrier (bgs_exact,
+// batch.cu): the wavefronts of the level's schedule cut into work items of at
+// most kExactItemRows rows, numbered in front order. Items are claimed by a
+// ticket; an item of front f starts once every item of front f-1 is done.
+// An item is one 256-thread CTA pass: 256 / (K/4) rows (32 rows for K <= 32,
+// 16 for K = 64, 8 for K = 128).
+constexpr int kMaxExactSweeps = 4;  // sweeps per launch (the counters cover them)
+struct ExactItems {
+  int32_t rows = 0;  // rows per item
+  int32_t nitems = 0, nfronts = 0;
+  DVec<int32_t> front, r0, r1;  // per item: its front and row range in sched.rows
+  DVec<int32_t> count;          // items per front
+};
+constexpr int kExactTables = 3;  // item tables of 32, 16 and 8 rows
+inline int exact_table_for(int K) { return K <= 32 ? 0 : K == 64 ? 1 : 2; }
+void build_exact_items(Ctx& c, const Schedule& sch, int32_t rows, ExactItems& out);
+
 struct DLevel {
   int kind = KIND_FINEST;
   DCSR op;
@@ -122,6 +139,7 @@ struct DLevel {
   std::unique_ptr<DDirect> direct;
   Schedule sched;          // exact-order GS wavefronts of this level's operator
   std::unique_ptr<DColor> color;  // throughput-mode coloured operator (on demand)
+  ExactItems xitems[kExactTables];  // throughput mode: exact-order K-column sweep items (per item size)
   LongRows blong_nat;             // throughput mode: long rows in natural order (K-column residuals)
   UpperIndex upper;        // energy / relaxation helpers
 };

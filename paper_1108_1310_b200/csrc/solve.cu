@@ -68,6 +68,7 @@ void Workspace::ensure(Ctx& c, const DHier& h, int K_) {
     w.x.alloc(n, c.s);
     w.r.alloc(n, c.s);
     if (L.direct) maxN = std::max(maxN, L.direct->maxN);
+    if (K_ > 1 && L.xitems[0].nitems) w.xctl.alloc(1 + (int64_t)kMaxExactSweeps * L.xitems[0].nfronts, c.s);
     if (l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_ELIM) {
       const auto& st = h.levels[l + 1]->stages;
       w.stage_rhs.resize(st.size());
@@ -252,7 +253,9 @@ struct Driver {
   }
   void visit_(size_t l, const double* b, double* x, int theta) {
     if (!exact && (int)l >= ws.tail.first) {
+      prof_mark(c, pcls(l, 3), true);
       ws.tail.run(c, (int)l, theta, cfg.mu, (int)h.levels.size());
+      prof_mark(c, pcls(l, 3), false);
       return;
     }
     const DLevel& L = *h.levels[l];
@@ -327,6 +330,7 @@ struct Driver {
     }
     if (l == 0) ws.top_rhs_valid = true;
     for (int i = 0; i < theta; ++i) {
+      prof_mark(c, pcls(l, 2), true);
       const double* cur = x;
       for (size_t s = 0; s < S; ++s) {
         double* out = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
@@ -334,8 +338,10 @@ struct Driver {
         else inject(c, st[s]->view(), cur, out);
         cur = out;
       }
+      prof_mark(c, pcls(l, 2), false);
       int theta_child = credits.take(l + 1, child.gamma);
       visit(l + 1, wc.b.p, wc.x.p, theta_child);
+      prof_mark(c, pcls(l, 2), true);
       for (size_t s = S; s-- > 0;) {
         const double* xc = s + 1 < S ? w.stage_x[s + 1].p : wc.x.p;
         double* out = s == 0 ? x : w.stage_x[s].p;
@@ -343,13 +349,15 @@ struct Driver {
         else backsub(c, st[s]->view(), xc, rhs[s], out);
         c.work += (double)st[s]->nnzf;
       }
+      prof_mark(c, pcls(l, 2), false);
     }
   }
 
-  // THROUGHPUT one-column solves sweep the c.exact_levels finest levels in the
-  // reference's exact order: on config 2 the finest level's order alone moves
-  // the cycle count from the reference's 129 to 141 coloured; exact on level 0
-  // restores 129 for ~5% more time per solve (the light wavefront kernel)
+  // THROUGHPUT solves (one column and K-column blocks) sweep the
+  // c.exact_levels finest levels in the reference's exact order: on config 2
+  // the finest level's order alone moves the cycle count from the
+  // reference's 129 to 141 coloured; exact on level 0 restores 129 (one
+  // column: the light wavefront kernel; blocks: bgs_exact's ticketed items)
   // levels below first_smooth + c.exact_levels sweep exactly, where
   // first_smooth is the finest level that smooths (level 0 on 3D grids; level
   // 1 when the finest is eliminated, as on RGG and 2D grids)
@@ -362,29 +370,36 @@ struct Driver {
       }
     return first + c.exact_levels;
   }
+  static int pcls(size_t l, int k) { return 2 + 4 * (int)std::min<size_t>(l, 63) + k; }
   void gs(size_t l, const double* b, double* x, int sweeps) {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 0, true);
+    prof_mark(c, pcls(l, 0), true);
     if (K > 1) {
       if (!L.color) throw LamgError(LAMG_E_ERROR, "batched smoothing needs the coloured operator");
-      bgs_colored(c, *L.color, L.op.n, b, x, sweeps, K);
+      const ExactItems& xi = L.xitems[exact_table_for(K)];
+      if ((int)l < exact_levels() && xi.nitems) bgs_exact(c, L.op.view(), L.sched, xi, b, x, sweeps, K, ws.lv[l].xctl.p);
+      else bgs_colored(c, *L.color, L.op.n, b, x, sweeps, K);
     } else if (!exact && L.color && (int)l >= exact_levels()) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
     else gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
     // algorithmic bytes: operator once (8(n+1) + 24m + 8n) + per column x
     // read, b read, x write (24n); K = 1 gives SURVEY.md 8(d)'s 24m + 40n + 8
     if (p) prof_mark(c, 0, false, (24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K) * sweeps);
+    prof_mark(c, pcls(l, 0), false, (24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K) * sweeps);
     c.work += (double)L.op.m * sweeps;
   }
   void resid(size_t l, const double* b, const double* x, double* r) {
     const DLevel& L = *h.levels[l];
     const bool p = l == 0;
     if (p) prof_mark(c, 1, true);
+    prof_mark(c, pcls(l, 1), true);
     if (K > 1) bresidual(c, L.op.view(), L.blong_nat, b, x, r, K);
     else if (!exact && has_long_rows(L.blong_nat)) residual_tasks(c, L.op.view(), L.blong_nat, b, x, r);
     else if (!exact && L.color) residual_tp(c, L.op.view(), b, x, r, *L.color);
     else residual_exact(c, L.op.view(), b, x, r, L.sched.heavy_nat.p, L.sched.nheavy_nat);
     if (p) prof_mark(c, 1, false, 24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K);
+    prof_mark(c, pcls(l, 1), false, 24.0 * L.op.m + 16.0 * L.op.n + 8.0 + 24.0 * L.op.n * K);
     c.work += (double)L.op.m;
   }
 
@@ -409,16 +424,20 @@ struct Driver {
         copy_d(c, w.saved_r[nsaved].p, w.r.p, L.op.n);
         ++nsaved;
       }
+      prof_mark(c, pcls(l, 2), true);
       if (K > 1) {
         brestrict(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p, wc.x.p, K);
       } else {
         restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p);
         wc.x.zero();
       }
+      prof_mark(c, pcls(l, 2), false);
       int theta_child = credits.take(l + 1, child.gamma);
       visit(l + 1, wc.b.p, wc.x.p, theta_child);
+      prof_mark(c, pcls(l, 2), true);
       if (K > 1) binterpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x, K);
       else interpolate(c, L.op.n, t.aggregate_of.p, wc.x.p, x);
+      prof_mark(c, pcls(l, 2), false);
       if (trace && K == 1) {
         resid(l, b, x, w.r.p);
         fprintf(stderr, "[trace]   l=%zu corrected |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
@@ -628,7 +647,7 @@ int solve_device(Ctx& c, const DHier& h, const double* b, const double* x0, cons
 // divergence) fires. A column's bits do not depend on the batch it rides in.
 int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const double* X0, const CycleCfg& cfg,
                        double* X, std::vector<SolveResult>& res) {
-  if (nrhs < 1 || nrhs > 32) throw LamgError(LAMG_E_ARGUMENT, "batched solve takes 1..32 right-hand sides");
+  if (nrhs < 1 || nrhs > kMaxBlock) throw LamgError(LAMG_E_ARGUMENT, "batched solve takes 1..128 right-hand sides");
   if (c.mode != LAMG_MODE_THROUGHPUT || cfg.correction != 0)
     throw LamgError(LAMG_E_ARGUMENT, "batched solve runs the flat THROUGHPUT cycle");
   const DLevel& L0 = *h.levels[0];
@@ -641,8 +660,9 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
   ws.ensure(c, h, K);
   ws.top_rhs_valid = false;
   if (!ws.tail_built) {
+    // levels of at most this many rows run in the K-column cluster tail
     const char* env = getenv("LAMG_BATCH_TAIL_ROWS");
-    ws.tail.build(c, h, ws, env ? atoi(env) : 40000);
+    ws.tail.build(c, h, ws, env ? atoi(env) : 16384);
     ws.tail_built = true;
   }
   ws.tail.reset(c);
@@ -653,17 +673,17 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
   to_node_major(c, X0, n, nrhs, K, Xw);
   // compatibility per column: |sum b| <= 1e-10 ||b||_inf
   unsigned long long* bmax = (unsigned long long*)c.dbscal;  // [K]
-  double* bsum = c.dbscal + 32;                              // [K]
-  double* rn_d = c.dbscal + 64;                              // [K]
-  double* xsum = c.dbscal + 96;                              // [K]
+  double* bsum = c.dbscal + kMaxBlock;                       // [K]
+  double* rn_d = c.dbscal + 2 * kMaxBlock;                   // [K]
+  double* xsum = c.dbscal + 3 * kMaxBlock;                   // [K]
   bcolabsmax(c, Bw, n, K, bmax);
   bcolsum(c, Bw, n, K, false, bsum);
-  CK(cudaMemcpyAsync(c.hscal, c.dbscal, 64 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  CK(cudaMemcpyAsync(c.hscal, c.dbscal, 2 * kMaxBlock * sizeof(double), cudaMemcpyDeviceToHost, c.s));
   c.sync();
   for (int j = 0; j < nrhs; ++j) {
     double b_inf;
     memcpy(&b_inf, &c.hscal[j], sizeof b_inf);
-    const double b_sum = c.hscal[32 + j];
+    const double b_sum = c.hscal[kMaxBlock + j];
     if (std::fabs(b_sum) > 1e-10 * b_inf)
       throw LamgError(LAMG_E_INCOMPATIBLE_RHS, "right-hand side sum " + to_string_f(b_sum) + " is not zero");
   }

@@ -40,6 +40,7 @@ struct LevelWS {
   DVec<double> b, x, r;
   std::vector<DVec<double>> stage_rhs, stage_x;  // index s >= 1
   DVec<double> saved_x[2], saved_r[2], tmp;
+  DVec<int32_t> xctl;  // bgs_exact ticket + per-front done counters (K > 1)
 };
 
 // per-context solve workspace, sized for the last hierarchy solved

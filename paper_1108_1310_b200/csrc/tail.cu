@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "batch.cuh"
 #include "solve.cuh"
@@ -41,6 +42,10 @@ struct GridScope {
   __device__ static void sync() { cg::this_cluster().sync(); }
   __device__ static bool leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
 };
+
+// K > 1, node-major, one CTA (small levels of the cluster tail: CTA 0 runs
+// them alone, a phase is a __syncthreads instead of a cluster barrier)
+struct CtaScope : BlockScope {};
 
 // ---------------------------------------------------------------- sweeps
 // shared-memory sweep (BlockScope only): every load of the sweep is an LDS
@@ -793,54 +798,449 @@ __device__ inline void cs_relax(const TLevel& L, const double* b, double* x, dou
   }
 }
 
+// ----------------------------------- K columns, node-major, one cluster
+// (batch.cuh) The block tail: the whole sub-cycle below the host-driven
+// levels for all K columns in ONE thread-block cluster (GridScope: a colour
+// phase costs one hardware cluster barrier), vectors node-major exactly as on
+// the host-driven levels, so the root needs no transposition. A (row, group
+// of 4 columns) pair is one thread: the row's entries are loaded once per
+// group and each x gather is one 256-bit access. Every column folds in the
+// row's entry (member, contribution) order -- the arithmetic of the batch.cu
+// kernels -- so a column's bits do not depend on K.
+template <bool SUB>
+__device__ __forceinline__ void nm_fold(double (&s)[kV], const int32_t* __restrict__ col,
+                                        const double* __restrict__ val, const double* X, int64_t e0, int64_t e1,
+                                        int K, int k0) {
+  constexpr int U = 8;
+  for (int64_t b = e0; b < e1; b += U) {
+    int32_t c[U];
+    double v[U];
+    d4 xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const bool ok = b + j < e1;
+      c[j] = ok ? __ldg(col + b + j) : 0;
+      v[j] = ok ? __ldg(val + b + j) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = b + j < e1 ? ld4(X + (int64_t)c[j] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (b + j < e1) {
+        if (SUB) {
+          s[0] = s[0] - v[j] * xv[j].x;
+          s[1] = s[1] - v[j] * xv[j].y;
+          s[2] = s[2] - v[j] * xv[j].z;
+          s[3] = s[3] - v[j] * xv[j].w;
+        } else {
+          s[0] = s[0] + v[j] * xv[j].x;
+          s[1] = s[1] + v[j] * xv[j].y;
+          s[2] = s[2] + v[j] * xv[j].z;
+          s[3] = s[3] + v[j] * xv[j].w;
+        }
+      }
+  }
+}
+__device__ __forceinline__ void nm_store(double* p, const double (&s)[kV], double d, const bool (&fz)[kV], bool any) {
+  if (!any) {
+    st4(p, s[0] / d, s[1] / d, s[2] / d, s[3] / d);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kV; ++q)
+      if (!fz[q]) p[q] = s[q] / d;
+  }
+}
+
+// Coloured sweep. Each thread's first row of the NEXT colour (row id, extent,
+// diagonal, b and the first 8 entries) is loaded before the barrier; after it
+// only the x gathers, the fold and the store remain.
+template <class S, int K>
+__device__ inline void nm_gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
+                             const int32_t* done, TailCounters* ctr) {
+  __shared__ int32_t s_cp[kMaxColors + 1];
+  if (L.ncolors == 0 || sweeps == 0) return;
+  constexpr int T = K / kV;
+  constexpr int U = 8;
+  const long long tg = clock64();
+  const int nc = L.ncolors;
+  const bool cached = nc <= kMaxColors;
+  if (cached)
+    for (int i = threadIdx.x; i <= nc; i += blockDim.x) s_cp[i] = __ldg(L.cptr + i);
+  __syncthreads();
+  const int64_t slot = S::tid() / T;
+  const int64_t rstride = S::stride() / T;
+  const int k0 = (int)(S::tid() % T) * kV;
+  bool fz[kV];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < kV; ++q) {
+    fz[q] = done && done[k0 + q];
+    any = any || fz[q];
+  }
+  const bool all = fz[0] && fz[1] && fz[2] && fz[3];
+  auto cbounds = [&](int cc, int32_t& c0, int32_t& c1) {
+    c0 = cached ? s_cp[cc] : __ldg(L.cptr + cc);
+    c1 = cached ? s_cp[cc + 1] : __ldg(L.cptr + cc + 1);
+  };
+  bool p_ok = false;
+  int32_t p_u = 0;
+  int64_t p_e0 = 0, p_e1 = 0;
+  double p_d = 1.0;
+  d4 p_b{0.0, 0.0, 0.0, 0.0};
+  int32_t p_c[U];
+  double p_v[U];
+  auto prefetch = [&](int cc) {
+    int32_t c0, c1;
+    cbounds(cc, c0, c1);
+    const int64_t i = c0 + slot;
+    p_ok = i < c1;
+    p_e0 = p_e1 = 0;
+    if (p_ok) {
+      p_u = __ldg(L.row_ids + i);
+      p_e0 = __ldg(L.prp + i);
+      p_e1 = __ldg(L.prp + i + 1);
+      p_d = __ldg(L.pdiag + i);
+      p_b = ld4(b + (int64_t)p_u * K + k0);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const bool ok = p_e0 + j < p_e1;
+      p_c[j] = ok ? __ldg(L.pcol + p_e0 + j) : 0;
+      p_v[j] = ok ? __ldg(L.pval + p_e0 + j) : 0.0;
+    }
+  };
+  prefetch(0);
+  long long a_first = 0, a_extra = 0, a_pre = 0, a_bar = 0;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int32_t cc = 0; cc < nc; ++cc) {
+      const long long tA = clock64();
+      int32_t i0, i1;
+      cbounds(cc, i0, i1);
+      if (p_ok && !all) {
+        d4 xv[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          xv[j] = p_e0 + j < p_e1 ? ld4(x + (int64_t)p_c[j] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
+        double sv[kV] = {p_b.x, p_b.y, p_b.z, p_b.w};
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (p_e0 + j < p_e1) {
+            sv[0] = sv[0] - p_v[j] * xv[j].x;
+            sv[1] = sv[1] - p_v[j] * xv[j].y;
+            sv[2] = sv[2] - p_v[j] * xv[j].z;
+            sv[3] = sv[3] - p_v[j] * xv[j].w;
+          }
+        if (p_e1 - p_e0 > U) nm_fold<true>(sv, L.pcol, L.pval, x, p_e0 + U, p_e1, K, k0);
+        nm_store(x + (int64_t)p_u * K + k0, sv, p_d, fz, any);
+      }
+      const long long tB = clock64();
+      if (!all)  // rows beyond each thread's first of this colour
+        for (int64_t i = i0 + slot + rstride; i < i1; i += rstride) {
+          const int32_t u = __ldg(L.row_ids + i);
+          const d4 bv = ld4(b + (int64_t)u * K + k0);
+          double sv[kV] = {bv.x, bv.y, bv.z, bv.w};
+          nm_fold<true>(sv, L.pcol, L.pval, x, __ldg(L.prp + i), __ldg(L.prp + i + 1), K, k0);
+          nm_store(x + (int64_t)u * K + k0, sv, __ldg(L.pdiag + i), fz, any);
+        }
+      const long long tC = clock64();
+      const int next = cc + 1 < nc ? cc + 1 : (sw + 1 < sweeps ? 0 : -1);
+      if (next >= 0) prefetch(next);
+      else p_ok = false;
+      const long long tD = clock64();
+      S::sync();
+      a_first += tB - tA;
+      a_extra += tC - tB;
+      a_pre += tD - tC;
+      a_bar += clock64() - tD;
+    }
+  if (S::leader()) {
+    ctr->lvl_ph[L.id][0] += a_first;
+    ctr->lvl_ph[L.id][1] += a_extra;
+    ctr->lvl_ph[L.id][2] += a_pre;
+    ctr->lvl_ph[L.id][3] += a_bar;
+    ctr->phases += (long long)sweeps * nc;
+    ctr->global_phases += (long long)sweeps * nc;
+    ctr->lvl_gs_cyc[L.id] += clock64() - tg;
+    ctr->lvl_gs_calls[L.id] += 1;
+  }
+}
+
+template <class S, int K>
+__device__ inline void nm_residual(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)L.n * T; t += S::stride()) {
+    const int64_t u = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const double d = __ldg(L.diag + u);
+    const d4 xu = ld4(x + u * K + k0);
+    double sv[kV] = {d * xu.x, d * xu.y, d * xu.z, d * xu.w};
+    nm_fold<false>(sv, L.col, L.val, x, __ldg(L.rp + u), __ldg(L.rp + u + 1), K, k0);
+    const d4 bv = ld4(b + u * K + k0);
+    st4(r + u * K + k0, bv.x - sv[0], bv.y - sv[1], bv.z - sv[2], bv.w - sv[3]);
+  }
+  S::sync();
+}
+
+template <class S, int K>
+__device__ inline void nm_restrict(const TLevel& L, const TLevel& C, const double* r, double mu) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)C.n * T; t += S::stride()) {
+    const int64_t g = t / T;
+    const int k0 = (int)(t % T) * kV;
+    double sv[kV] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j = __ldg(L.mem_ptr + g); j < __ldg(L.mem_ptr + g + 1); ++j) {
+      const d4 rv = ld4(r + (int64_t)__ldg(L.mem + j) * K + k0);
+      sv[0] = sv[0] + rv.x;
+      sv[1] = sv[1] + rv.y;
+      sv[2] = sv[2] + rv.z;
+      sv[3] = sv[3] + rv.w;
+    }
+    if (mu != 1.0) st4(C.b + g * K + k0, sv[0] * mu, sv[1] * mu, sv[2] * mu, sv[3] * mu);
+    else st4(C.b + g * K + k0, sv[0], sv[1], sv[2], sv[3]);
+    st4(C.x + g * K + k0, 0.0, 0.0, 0.0, 0.0);
+  }
+  S::sync();
+}
+
+template <class S, int K>
+__device__ inline void nm_interp(const TLevel& L, const TLevel& C, double* x) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)L.n * T; t += S::stride()) {
+    const int64_t u = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const d4 xv = ld4(x + u * K + k0);
+    const d4 cv = ld4(C.x + (int64_t)__ldg(L.agg + u) * K + k0);
+    st4(x + u * K + k0, xv.x + cv.x, xv.y + cv.y, xv.z + cv.z, xv.w + cv.w);
+  }
+  S::sync();
+}
+
+template <class S, int K>
+__device__ inline void nm_coarsen(const StageV& s, const double* b, double* bc) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
+    const int64_t q = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const d4 bv = ld4(b + (int64_t)__ldg(s.poc + q) * K + k0);
+    double v[kV] = {bv.x, bv.y, bv.z, bv.w};
+    for (int64_t j = __ldg(s.t_ptr + q); j < __ldg(s.t_ptr + q + 1); ++j) {
+      const int64_t p = __ldg(s.t_p + j);
+      const int32_t i = __ldg(s.f_of_p + p);
+      const double fv = __ldg(s.f_val + p), fd = __ldg(s.f_diag + i);
+      const d4 fb = ld4(b + (int64_t)__ldg(s.f_nodes + i) * K + k0);
+      v[0] = v[0] - fv * (fb.x / fd);
+      v[1] = v[1] - fv * (fb.y / fd);
+      v[2] = v[2] - fv * (fb.z / fd);
+      v[3] = v[3] - fv * (fb.w / fd);
+    }
+    st4(bc + q * K + k0, v[0], v[1], v[2], v[3]);
+  }
+  S::sync();
+}
+
+template <class S, int K>
+__device__ inline void nm_inject(const StageV& s, const double* x, double* xc) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
+    const int64_t q = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const d4 v = ld4(x + (int64_t)__ldg(s.poc + q) * K + k0);
+    st4(xc + q * K + k0, v.x, v.y, v.z, v.w);
+  }
+  S::sync();
+}
+
+template <class S, int K>
+__device__ inline void nm_backsub(const StageV& s, const double* xc, const double* b, double* x) {
+  constexpr int T = K / kV;
+  for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
+    const int64_t q = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const d4 v = ld4(xc + q * K + k0);
+    st4(x + (int64_t)__ldg(s.poc + q) * K + k0, v.x, v.y, v.z, v.w);
+  }
+  S::sync();
+  for (int64_t t = S::tid(); t < (int64_t)s.nf * T; t += S::stride()) {
+    const int64_t i = t / T;
+    const int k0 = (int)(t % T) * kV;
+    const int32_t f = __ldg(s.f_nodes + i);
+    const d4 bv = ld4(b + (int64_t)f * K + k0);
+    double sv[kV] = {bv.x, bv.y, bv.z, bv.w};
+    for (int64_t p = __ldg(s.f_ptr + i); p < __ldg(s.f_ptr + i + 1); ++p) {
+      const double fv = __ldg(s.f_val + p);
+      const d4 xv = ld4(x + (int64_t)__ldg(s.f_nbr + p) * K + k0);
+      sv[0] = sv[0] - fv * xv.x;
+      sv[1] = sv[1] - fv * xv.y;
+      sv[2] = sv[2] - fv * xv.z;
+      sv[3] = sv[3] - fv * xv.w;
+    }
+    const double d = __ldg(s.f_diag + i);
+    st4(x + (int64_t)f * K + k0, sv[0] / d, sv[1] / d, sv[2] / d, sv[3] / d);
+  }
+  S::sync();
+}
+
+// X = Minv[:n,:n] B per component (the throughput inverse; bdirect's order)
+template <class S, int K>
+__device__ inline void nm_direct(const TLevel& L, const double* b, double* x) {
+  constexpr int T = K / kV;
+  for (int32_t ci = 0; ci < L.ncomp; ++ci) {
+    const int32_t s0 = __ldg(L.comp_start + ci), cn = __ldg(L.comp_start + ci + 1) - s0;
+    const double* Mi = L.inv + __ldg(L.inv_off + ci);
+    for (int64_t t = S::tid(); t < (int64_t)cn * T; t += S::stride()) {
+      const int32_t i = (int32_t)(t / T);
+      const int k0 = (int)(t % T) * kV;
+      double sv[kV] = {0.0, 0.0, 0.0, 0.0};
+      for (int32_t j = 0; j < cn; ++j) {
+        const double m = __ldg(Mi + (int64_t)i * cn + j);
+        const d4 bv = ld4(b + (int64_t)(L.whole ? j : __ldg(L.nodes + s0 + j)) * K + k0);
+        sv[0] += m * bv.x;
+        sv[1] += m * bv.y;
+        sv[2] += m * bv.z;
+        sv[3] += m * bv.w;
+      }
+      st4(x + (int64_t)(L.whole ? i : __ldg(L.nodes + s0 + i)) * K + k0, sv[0], sv[1], sv[2], sv[3]);
+    }
+  }
+  S::sync();
+}
+
+// per-column sums over the cluster in a K-independent order (kChunks chunks
+// of R rows folded in sequence, chunk sums folded in sequence); every CTA
+// gets all K sums in s_out (shared memory)
+template <class S, int K, bool SQ>
+__device__ inline void nm_colsum(const double* X, int64_t n, double* part, double* s_out) {
+  const int64_t R = (n + kChunks - 1) / kChunks;
+  const int np = (int)((n + R - 1) / R);
+  for (int64_t t = S::tid(); t < (int64_t)np * K; t += S::stride()) {
+    const int64_t p = t / K;
+    const int k = (int)(t % K);
+    const int64_t u1 = (p + 1) * R < n ? (p + 1) * R : n;
+    double s = 0.0;
+    for (int64_t u = p * R; u < u1; ++u) {
+      const double v = X[u * K + k];
+      s += SQ ? v * v : v;
+    }
+    part[(int64_t)k * kChunks + p] = s;
+  }
+  S::sync();
+  if ((int)threadIdx.x < K) {
+    double tot = 0.0;
+    for (int p = 0; p < np; ++p) tot += ((volatile double*)part)[(int64_t)threadIdx.x * kChunks + p];
+    s_out[threadIdx.x] = tot;
+  }
+  S::sync();  // part is reused by the next sum
+}
+
+// RelaxationSolver::solve (coarse_solver.cpp:82-93) per column; each column
+// freezes at its own tolerance
+template <class S, int K>
+__device__ inline void nm_relax(const TLevel& L, const double* b, double* x, double* part, TailCounters* ctr) {
+  __shared__ int32_t s_done[kMaxBlock];
+  __shared__ double s_r0[kMaxBlock], s_sum[kMaxBlock];
+  constexpr int T = K / kV;
+  const int64_t n = L.n;
+  nm_residual<S, K>(L, b, x, L.r);
+  nm_colsum<S, K, true>(L.r, n, part, s_sum);
+  if ((int)threadIdx.x < K) {
+    s_r0[threadIdx.x] = sqrt(s_sum[threadIdx.x]);
+    s_done[threadIdx.x] = s_r0[threadIdx.x] == 0.0;
+  }
+  __syncthreads();
+  if (S::leader()) ctr->work += (double)L.m;
+  for (int sweep = 0; sweep < 400; ++sweep) {
+    int active = 0;
+    for (int k = 0; k < K; ++k) active += !s_done[k];
+    if (!active) break;
+    nm_gs<S, K>(L, b, x, 1, s_done, ctr);
+    nm_colsum<S, K, false>(x, n, part, s_sum);
+    for (int64_t t = S::tid(); t < n * T; t += S::stride()) {
+      const int64_t u = t / T;
+      const int k0 = (int)(t % T) * kV;
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+        if (!s_done[k0 + q]) x[u * K + k0 + q] -= s_sum[k0 + q] / (double)n;
+    }
+    S::sync();
+    nm_residual<S, K>(L, b, x, L.r);
+    nm_colsum<S, K, true>(L.r, n, part, s_sum);
+    if (S::leader()) {
+      ctr->work += 2.0 * (double)L.m;
+      ctr->relax_sweeps += 1;
+    }
+    if ((int)threadIdx.x < K && !s_done[threadIdx.x] && sqrt(s_sum[threadIdx.x]) <= 1e-12 * s_r0[threadIdx.x])
+      s_done[threadIdx.x] = 1;
+    __syncthreads();
+  }
+}
+
 // single-column (any scope) or K-column column-slice (CTA scope) form of each
 // operation of the recursion
 template <class S, int K>
 __device__ inline void op_gs(const TLevel& L, const double* b, double* x, int sweeps, TailCounters* ctr,
                              int32_t xs_rows) {
-  if constexpr (K == 1) gs<S>(L, b, x, sweeps, ctr, xs_rows);
+  if constexpr (K == 1) {
+    gs<S>(L, b, x, sweeps, ctr, xs_rows);
+  } else if constexpr (std::is_same<S, GridScope>::value) {
+    if (L.gs_cta) {  // small level: CTA 0 sweeps, the cluster waits once
+      if (blockIdx.x == 0) nm_gs<CtaScope, K>(L, b, x, sweeps, nullptr, ctr);
+      GridScope::sync();
+    } else {
+      nm_gs<GridScope, K>(L, b, x, sweeps, nullptr, ctr);
+    }
+  } else if constexpr (std::is_same<S, CtaScope>::value) {
+    nm_gs<CtaScope, K>(L, b, x, sweeps, nullptr, ctr);
+  }
   else if (L.smem_cs) cs_gs_smem<K>(L, b, x, sweeps, ctr);
   else cs_gs<K>(L, b, x, sweeps, nullptr, ctr);
 }
 template <class S, int K>
 __device__ inline void op_residual(const TLevel& L, const double* b, const double* x, double* r) {
   if constexpr (K == 1) residual<S>(L, b, x, r);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_residual<S, K>(L, b, x, r);
   else cs_residual<K>(L, b, x, r);
 }
 template <class S, int K>
 __device__ inline void op_restrict(const TLevel& L, const TLevel& C, const double* r, double mu) {
   if constexpr (K == 1) restrict_to<S>(L, C, r, mu);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_restrict<S, K>(L, C, r, mu);
   else cs_restrict<K>(L, C, r, mu);
 }
 template <class S, int K>
 __device__ inline void op_interp(const TLevel& L, const TLevel& C, double* x) {
   if constexpr (K == 1) interpolate<S>(L, C, x);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_interp<S, K>(L, C, x);
   else cs_interp<K>(L, C, x);
 }
 template <class S, int K>
 __device__ inline void op_coarsen(const StageV& s, const double* b, double* bc) {
   if constexpr (K == 1) coarsen<S>(s, b, bc);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_coarsen<S, K>(s, b, bc);
   else cs_coarsen<K>(s, b, bc);
 }
 template <class S, int K>
 __device__ inline void op_inject(const StageV& s, const double* x, double* xc) {
   if constexpr (K == 1) inject<S>(s, x, xc);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_inject<S, K>(s, x, xc);
   else cs_inject<K>(s, x, xc);
 }
 template <class S, int K>
 __device__ inline void op_backsub(const StageV& s, const double* xc, const double* b, double* x) {
   if constexpr (K == 1) backsub<S>(s, xc, b, x);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_backsub<S, K>(s, xc, b, x);
   else cs_backsub<K>(s, xc, b, x);
 }
 template <class S, int K>
 __device__ inline void op_direct(const TLevel& L, const double* b, double* x) {
   if constexpr (K == 1) direct(L, b, x);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_direct<S, K>(L, b, x);
   else cs_direct<K>(L, b, x);
 }
 template <class S, int K>
 __device__ inline void op_relax(const TLevel& L, const double* b, double* x, double* sh, double* part,
                                 TailCounters* ctr, int32_t xs_rows) {
   if constexpr (K == 1) relax<S>(L, b, x, sh, part, ctr, xs_rows);
+  else if constexpr (!std::is_same<S, BlockScope>::value) nm_relax<S, K>(L, b, x, part, ctr);
   else cs_relax<K>(L, b, x, part, ctr);
 }
 
@@ -871,7 +1271,9 @@ __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, doubl
                                      int32_t small_rows, double* sh, double* part, TailCounters* ctr,
                                      int32_t xs_rows) {
   if (levels[f.l].n > small_rows) return false;
-  if (blockIdx.x == 0) visit_loop<BlockScope, K>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
+  // K > 1: CTA 0 runs the small subtree for all K columns, node-major
+  using Small = typename std::conditional<K == 1, BlockScope, CtaScope>::type;
+  if (blockIdx.x == 0) visit_loop<Small, K>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
   GridScope::sync();
   return true;
 }
@@ -879,7 +1281,6 @@ __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, doubl
 template <class S, int K>
 __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0, double* credits, double mu,
                            int32_t small_rows, double* sh, double* part, TailCounters* ctr, int32_t xs_rows) {
-  static_assert(K == 1 || std::is_same<S, BlockScope>::value, "K-column blocks run in CTA scope only");
   Frame st[kMaxLevels];
   int sp = 0;
   st[sp++] = Frame{l0, theta0, 0, 0};
@@ -1018,8 +1419,12 @@ __global__ void __launch_bounds__(kTailThreadsBatch, 1) subtree_kernel(const TLe
 
 void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   const int nl = (int)h.levels.size();
-  subtree = ws.K > 1;
-  if (subtree) {  // blocks of columns: the tail is the small-level subtree
+  // blocks of columns: by default the node-major cluster tail (nm_* ops);
+  // LAMG_BATCH_TAIL=subtree selects the per-column CTA subtree below 4096 rows
+  const char* et = getenv("LAMG_BATCH_TAIL");
+  subtree = ws.K > 1 && ws.K <= 32 && et && strcmp(et, "subtree") == 0;
+  const bool nm = ws.K > 1 && !subtree;
+  if (subtree) {
     const char* eb = getenv("LAMG_BATCH_SMALL");
     max_rows = eb ? atoi(eb) : 4096;
   }
@@ -1041,8 +1446,16 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   // neutral on cfg2: the phases are bound by the L2 chain of the operator rows)
   const char* e5 = getenv("LAMG_TAIL_XSMEM");
   xs_rows = (e5 && atoi(e5) == 1) ? small_rows : 0;
-  const char* e2 = getenv("LAMG_TAIL_CTAS");
-  ctas = std::max(1, std::min(e2 ? atoi(e2) : 8, 16));  // one cluster (<= 16 CTAs)
+  const char* e2 = getenv(nm ? "LAMG_BATCH_CTAS" : "LAMG_TAIL_CTAS");
+  ctas = std::max(1, std::min(e2 ? atoi(e2) : (nm ? 16 : 8), 16));  // one cluster (<= 16 CTAs)
+  if (nm) {
+    // subtrees rooted at levels of at most this many rows run in CTA 0 alone
+    // (a phase is a __syncthreads instead of a cluster barrier)
+    const char* es = getenv("LAMG_BATCH_SMALL");
+    small_rows = es ? atoi(es) : 0;
+    smem = 0;
+    xs_rows = 0;
+  }
   std::vector<TLevel> tl(nl);
   for (int l = first; l < nl; ++l) {
     const DLevel& L = *h.levels[l];
@@ -1083,7 +1496,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
       t.inv = d.inv.p;
       t.inv_off = d.inv_off.p;
       t.whole = d.ncomp == 1;
-      if (a.n > small_rows) small_rows = a.n;  // the direct coarsest runs in one CTA
+      if (!nm && a.n > small_rows) small_rows = a.n;  // the one-column direct coarsest runs in one CTA
     }
     if (l + 1 < nl && L.coarsest == CM_NONE) {
       const DLevel& C = *h.levels[l + 1];
@@ -1113,7 +1526,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     smem = std::min(smem, kTailSmemMax);
   }
   K = ws.K;
-  if (K > 1) {  // column-slice sweeps stage operator + slice in shared memory
+  if (subtree) {  // column-slice sweeps stage operator + slice in shared memory
     const char* e6 = getenv("LAMG_BATCH_SMEM_KB");
     smem = std::min(kTailSmemMax, (e6 ? atoi(e6) : 200) * 1024);
   }
@@ -1132,14 +1545,16 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     case 1: kernel = occ2 ? (const void*)tail_kernel<2, 1> : (const void*)tail_kernel<1, 1>; break;
     // K > 1: 256 threads (255 registers) -- the column-slice phases are
     // latency-bound chains, more warps per CTA only add issue overhead
-    case 4: kernel = (const void*)subtree_kernel<4>; break;
-    case 8: kernel = (const void*)subtree_kernel<8>; break;
+    case 4: kernel = subtree ? (const void*)subtree_kernel<4> : (const void*)tail_kernel<1, 4, kTailThreadsBatch>; break;
+    case 8: kernel = subtree ? (const void*)subtree_kernel<8> : (const void*)tail_kernel<1, 8, kTailThreadsBatch>; break;
     case 16:
-      kernel = (const void*)subtree_kernel<16>;
+      kernel = subtree ? (const void*)subtree_kernel<16> : (const void*)tail_kernel<1, 16, kTailThreadsBatch>;
       break;
     case 32:
-      kernel = (const void*)subtree_kernel<32>;
+      kernel = subtree ? (const void*)subtree_kernel<32> : (const void*)tail_kernel<1, 32, kTailThreadsBatch>;
       break;
+    case 64: kernel = (const void*)tail_kernel<1, 64, kTailThreadsBatch>; break;
+    case 128: kernel = (const void*)tail_kernel<1, 128, kTailThreadsBatch>; break;
     default: throw LamgError(LAMG_E_ARGUMENT, "tail: unsupported batch width");
   }
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax));
@@ -1163,13 +1578,18 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     ctas /= 2;
   }
   part.alloc(std::max<int64_t>(std::max(ctas, 1), kChunks) * K, c.s);
-  if (K > 1) {
+  if (subtree) {
     const int kc = K >= ctas ? K / ctas : 1;
     for (int l = first; l < nl; ++l) {
       const DLevel& L = *h.levels[l];
       tl[l].smem_cs = L.color && L.op.n <= small_rows &&
                       cs_smem_bytes(L.op.n, 2 * L.op.m, L.color->ncolors, kc) <= smem;
     }
+  }
+  if (nm) {  // LAMG_BATCH_GS_CTA=rows: sweeps of levels this small run in CTA 0 (tools/micro/phase_bench)
+    const char* eg = getenv("LAMG_BATCH_GS_CTA");
+    const int32_t gs_rows = eg ? atoi(eg) : 0;  // off: slower in the full kernel (extra-row chains)
+    for (int l = first; l < nl; ++l) tl[l].gs_cta = h.levels[l]->op.n <= gs_rows;
   }
   if (subtree) {  // column-major copies of the root level's b and x (see subtree_kernel)
     const int64_t rn = (int64_t)h.levels[first]->op.n * K;

@@ -43,6 +43,8 @@ struct TLevel {
   int group;    // lanes per row (1, 4, 8)
   int smem_ok;  // the coloured operator + x + b fit the tail CTA's shared memory
   int smem_cs;  // K > 1: the operator + this CTA's column slice of x and b fit
+  int gs_cta;   // K > 1 cluster tail: this level's sweeps run in CTA 0 alone (a
+                // __syncthreads per colour instead of a cluster barrier)
   // workspace
   double* b;
   double* x;

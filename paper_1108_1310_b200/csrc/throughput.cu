@@ -955,6 +955,8 @@ void prepare_throughput(Ctx& c, DHier& h) {
     const bool smooths = (L.coarsest == CM_RELAX) ||
                          (L.coarsest == CM_NONE && l + 1 < h.levels.size() && h.levels[l + 1]->kind == KIND_AGG);
     if (smooths && !L.color) L.color = make_color(c, L.op.view(), L.sched);
+    if (smooths && L.coarsest == CM_NONE && !L.xitems[0].rows)
+      for (int t = 0; t < kExactTables; ++t) build_exact_items(c, L.sched, 32 >> t, L.xitems[t]);
     if (L.direct) build_direct_inverse(c, *L.direct);
     build_natural_long_rows(c, L.op.view(), L.blong_nat);
   }
@@ -972,6 +974,32 @@ std::unique_ptr<DColor> make_color(Ctx& c, const CSRv& a, const Schedule& sch) {
   col->rp = std::move(rp2);
   c.sync();
   return col;
+}
+
+void build_exact_items(Ctx& c, const Schedule& sch, int32_t rows, ExactItems& out) {
+  const std::vector<int32_t> fp = sch.front_ptr.to_host();
+  std::vector<int32_t> fr, r0, r1, cnt(sch.nfronts, 0);
+  for (int32_t f = 0; f < sch.nfronts; ++f)
+    for (int32_t i = fp[f]; i < fp[f + 1]; i += rows) {
+      fr.push_back(f);
+      r0.push_back(i);
+      r1.push_back(std::min(i + rows, fp[f + 1]));
+      ++cnt[f];
+    }
+  out.rows = rows;
+  out.nitems = (int32_t)fr.size();
+  out.nfronts = sch.nfronts;
+  out.front.alloc(std::max<int64_t>(1, out.nitems), c.s);
+  out.r0.alloc(std::max<int64_t>(1, out.nitems), c.s);
+  out.r1.alloc(std::max<int64_t>(1, out.nitems), c.s);
+  out.count.alloc(std::max(1, sch.nfronts), c.s);
+  if (out.nitems) {
+    out.front.upload(fr.data(), out.nitems);
+    out.r0.upload(r0.data(), out.nitems);
+    out.r1.upload(r1.data(), out.nitems);
+    out.count.upload(cnt.data(), sch.nfronts);
+  }
+  c.sync();
 }
 
 void build_natural_long_rows(Ctx& c, const CSRv& a, LongRows& out) {

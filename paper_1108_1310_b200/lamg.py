@@ -348,6 +348,14 @@ class Hierarchy:
                                              C.c_int32(sweeps)))
         return x
 
+    def smooth_exact(self, l: int, b, x, sweeps: int = 1):
+        """`sweeps` Gauss-Seidel sweeps on level l in the reference's row order; b, x are [n] or node-major [n, K]."""
+        b, x = np.ascontiguousarray(b, np.float64), np.array(x, np.float64, order="C")
+        k = 1 if x.ndim == 1 else x.shape[1]
+        _check(self.ctx.lib.lamg_hier_smooth_exact(self.ctx.p, self.h, C.c_int32(l), C.c_int32(k), _p(b), _p(x),
+                                                   C.c_int32(sweeps)))
+        return x
+
     def solve(self, b, x0, **cycle):
         """Oracle-style solve: returns (x, stats dict); errors carry .stats."""
         cfg = CycleConfig(**{k: v for k, v in cycle.items() if k != "seed"})
@@ -470,7 +478,7 @@ def solve(h: Hierarchy, b, x0, cfg: CycleConfig | None = None, ctx: Context | No
 def solve_batch(h: Hierarchy, B, X0, cfg: CycleConfig | None = None, ctx: Context | None = None):
     """nrhs independent solves (one lamg::solve per row of B, cycle.cpp:221-273).
 
-    B and X0 are [nrhs, n]. THROUGHPUT mode runs blocks of up to 32 columns
+    B and X0 are [nrhs, n]. THROUGHPUT mode runs blocks of up to 128 columns
     through one cycle schedule (lamg_solve_batch); VALIDATE mode solves each
     column in the reference's order. Returns (X [nrhs, n], [SolveStats]).
     """

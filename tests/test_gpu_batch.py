@@ -4,8 +4,10 @@ The reference solves one b per lamg::solve call (cycle.cpp:221-273); a batch
 is nrhs such calls on one hierarchy. VALIDATE mode must return, per column,
 exactly what the single solve returns (bit-identical to the reference).
 THROUGHPUT mode runs up to 32 columns through one cycle schedule; per column
-it must converge to the reference tolerance (r <= r0/1e10), land within
-1e-7 relative of the reference solution, and -- because every kernel folds a
+it must converge to the reference tolerance (r <= r0/1e10) in the reference's
+cycle count +-1, land within 1e-8 relative of the reference solution (the
+finest smoothing level is swept in the reference's order by bgs_exact), and
+-- because every kernel folds a
 column independently of the others -- give the same bits whatever the
 batch it rides in.
 """
@@ -64,8 +66,9 @@ def test_throughput_batch_converges_to_reference_solution(problem):
         s = st[j]
         assert s.converged and s.residuals[-1] <= s.residuals[0] / 1e10, (name, j)
         assert s.residuals[0] == pytest.approx(sr.residuals[0], rel=1e-12)
-        assert np.linalg.norm(X[j] - xr) / np.linalg.norm(xr) <= 1e-7, (name, j)
-        assert abs(s.cycles - sr.cycles) <= max(3, sr.cycles // 5), (name, j, s.cycles, sr.cycles)
+        # north_star's solve rule: the reference's cycle count +-1, x within 1e-8
+        assert np.linalg.norm(X[j] - xr) / np.linalg.norm(xr) <= 1e-8, (name, j)
+        assert abs(s.cycles - sr.cycles) <= 1, (name, j, s.cycles, sr.cycles)
 
 
 def test_throughput_column_independent_of_batch(problem):
@@ -79,6 +82,24 @@ def test_throughput_column_independent_of_batch(problem):
         for i, j in enumerate(idx):
             assert np.array_equal(Xs[i], X32[j]), (idx, j)
             assert ss[i].residuals == s32[j].residuals
+
+
+def test_throughput_wide_blocks_equal_narrow_blocks(problem):
+    # 64- and 128-column blocks run the same per-column arithmetic (one cycle
+    # schedule, entry-order folds) as 32-column blocks: identical bits
+    from paper_1108_1310_b200 import lamg as L
+    _, a, ctx, h = problem
+    ctx.set_mode(L.MODE_THROUGHPUT)
+    B, X0 = rhs_block(a.n, 72)
+    X32, s32 = L.solve_batch(h, B[:32], X0[:32], ctx=ctx)
+    X72, s72 = L.solve_batch(h, B, X0, ctx=ctx)  # one 128-wide block
+    X40, s40 = L.solve_batch(h, B[32:72], X0[32:72], ctx=ctx)  # one 64-wide block
+    for j in range(32):
+        assert np.array_equal(X72[j], X32[j]), j
+        assert s72[j].residuals == s32[j].residuals
+    for j in range(40):
+        assert np.array_equal(X72[32 + j], X40[j]), j
+        assert s72[32 + j].cycles == s40[j].cycles
 
 
 def test_throughput_batch_zero_and_incompatible_rhs(problem):
