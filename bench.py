@@ -2,12 +2,15 @@
 """Benchmark of the B200 LAMG hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lamg|reference]
-                    [--mode throughput|validate] [--config 2] [--lanes 4] [--block 32]
+                    [--mode throughput|validate] [--config 1..5] [--lanes 8] [--block 32]
 
-A step solves lanes x block right-hand sides (default 4 x 32), each to the
+A step solves lanes x block right-hand sides (default 8 x 32), each to the
 reference's relative residual 1e-10, on BASELINE.json config 2 -- the 3D
 7-point 128^3 Laplacian with seeded log-uniform weights -- over a hierarchy
-built once on the GPU (setup is timed separately and reported). Each lane is
+built once on the GPU (setup is timed separately and reported; configs 4 and
+5 are generated on the device). With --gpus N and no WORLD_SIZE in the
+environment, bench.py relaunches itself under torch.distributed.run with N
+ranks (127.0.0.1, NCCL_DEBUG=INFO). Each lane is
 one lamg_solve_batch_dev call on its own stream; the single-RHS solve time is
 reported beside it. `value` is fine-level edges*cycles/s of the
 whole job (sum over ranks of m1 * cycles per step / max-over-ranks device
@@ -104,15 +107,57 @@ class ClockSampler:
 WORKLOADS = {
     1: "cfg1: 2D 5-point grid 256^2 (n=65,536), unit weights, Gaussian zero-sum b, to 1e-10",
     2: "cfg2: 3D 7-point grid 128^3 (n=2,097,152, m=6,242,304), weights 10^U[-3,3], Gaussian zero-sum b, to 1e-10",
+    3: "cfg3: random geometric graph, 4M points in the unit square, mean degree ~10, weights 1/distance, largest "
+       "component, Gaussian zero-sum b, to 1e-10",
+    4: "cfg4: Chung-Lu power law n=16M, exponent 2.1, mean degree 16, unit weights, largest component (generated on "
+       "the device), Gaussian zero-sum b, to 1e-10",
+    5: "cfg5: R-MAT scale 25, edge factor 16, (0.57,0.19,0.19,0.05), summed weights, largest component (generated on "
+       "the device), Gaussian zero-sum b, to 1e-10",
 }
+DEFAULT_LANES = {1: 8, 2: 8, 3: 8, 4: 2, 5: 2}
 
 
-def build_inputs(cfg: int, rank: int):
+def rhs_seed(cfg: int, rank: int, i: int) -> int:
+    """Seed of right-hand side i of a rank; the reference arm solves the same b's."""
+    return 100 + cfg + 1000 * rank + 7 * i
+
+
+def x0_seed(rank: int, i: int) -> int:
+    return 1 + rank + 97 * i
+
+
+def build_operator(cfg: int, ctx=None):
+    """Host CSR of a config (configs 4 and 5: generated on the device with
+    ctx, bit-identical to the host generators; returned as a DeviceGraph)."""
     from paper_1108_1310_b200 import graphs as G
-    a = G.make_config(cfg)
-    b = G.gaussian_rhs(a.n, 100 + cfg + 1000 * rank)
-    x0 = G.default_x0(a.n, seed=1 + rank)
-    return a, b, x0
+    from paper_1108_1310_b200 import lamg as L
+    if cfg == 4 and ctx is not None:
+        return L.gen_chung_lu(1 << 24, seed=4, ctx=ctx)
+    if cfg == 5 and ctx is not None:
+        return L.gen_rmat(25, seed=5, ctx=ctx)
+    return G.make_config(cfg)
+
+
+def zero_sum(B):
+    """At n ~ 1e7 the sequential mean subtraction of gaussian_rhs leaves |sum b|
+    near the reference's 1e-10 * max|b| compatibility threshold
+    (cycle.cpp:226-230): project again with a pairwise sum."""
+    for _ in range(2):
+        B -= (B.sum(axis=-1, keepdims=True) / B.shape[-1])
+    return B
+
+
+def cpu_info() -> dict:
+    info = {"threads": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Thread(s) per core", "Socket(s)", "Core(s) per socket"):
+                info[k.strip()] = v.strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return info
 
 
 def sha(a) -> str:
@@ -153,6 +198,10 @@ class Lane:
     def _done(self, code):
         self.L._check(code)
         self.cycles = [int(self.st[j].cycles) for j in range(self.k)]
+        self.sweeps = [int(self.st[j].relax_sweeps) for j in range(self.k)]
+
+    def sweeps_total(self):
+        return sum(getattr(self, "sweeps", [0]))
 
     def solve_dev(self):
         try:
@@ -228,6 +277,21 @@ def kernel_profile(lib, lane, fn, ms_total):
     return kern
 
 
+def relax_info(h, relax_levels, sweeps_per_s, hbm, K):
+    """Configs 4/5 end in a relaxation-coarsest level whose coloured sweeps are
+    the whole solve: edges*sweeps/s there, and the HBM rate those sweeps imply
+    (per sweep and per residual: operator 24m + 16n + 8 once, 24n per column)."""
+    if not relax_levels:
+        return None
+    li = h.levels[relax_levels[0]]
+    per_sweep = 24.0 * li.m + 16.0 * li.n + 8.0 + 24.0 * li.n * K
+    # one sweep + one residual per relaxation sweep (coarse_solver.cpp:82-93)
+    gbs = sweeps_per_s / li.m / K * 2 * per_sweep / 1e9 if li.m else 0.0
+    return {"level": relax_levels[0], "n": li.n, "m": li.m, "edges_sweeps_per_s": sweeps_per_s,
+            "implied_gbs": round(gbs, 1), "frac_of_hbm": round(gbs / hbm, 4),
+            "bytes": "per sweep and per residual of a K-column block: 24m + 16n + 8 + 24nK (K = 1: 24m + 40n + 8)"}
+
+
 def run_lamg(args, dist: Dist):
     import torch
     from paper_1108_1310_b200 import graphs as G
@@ -235,25 +299,34 @@ def run_lamg(args, dist: Dist):
 
     dev = dist.local
     torch.cuda.set_device(dev)
-    NL, KB = args.lanes, args.block
-    t0 = time.time()
-    a, b, x0 = build_inputs(args.config, dist.rank)
-    nrhs = NL * KB
-    B = np.stack([b] + [G.gaussian_rhs(a.n, 100 + args.config + 1000 * dist.rank + 7 * i) for i in range(1, nrhs)])
-    X0 = np.stack([x0] + [G.default_x0(a.n, seed=1 + dist.rank + 97 * i) for i in range(1, nrhs)])
-    log(f"[rank {dist.rank}] inputs n={a.n} m={a.m} ({NL} lanes x {KB} right-hand sides) built in "
-        f"{time.time() - t0:.1f}s")
+    NL, KB = args.lanes or DEFAULT_LANES[args.config], args.block
     mode = L.MODE_THROUGHPUT if args.mode == "throughput" else L.MODE_VALIDATE
     ctx0 = L.Context(dev, mode)
     lib = ctx0.lib
+    t0 = time.time()
+    a = build_operator(args.config, ctx0)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    nrhs = NL * KB
+    B = np.stack([G.gaussian_rhs(a.n, rhs_seed(args.config, dist.rank, i)) for i in range(nrhs)])
+    X0 = np.stack([G.default_x0(a.n, seed=x0_seed(dist.rank, i)) for i in range(nrhs)])
+    if args.config >= 4:
+        B = zero_sum(B)
+    b, x0 = B[0], X0[0]
+    ha = a.download() if hasattr(a, "download") else a  # host copy for the CPU baseline
+    log(f"[rank {dist.rank}] inputs n={a.n} m={a.m} ({NL} lanes x {KB} right-hand sides) built in "
+        f"{time.time() - t0:.1f}s (operator {gen_s:.1f}s)")
     torch.cuda.synchronize()
     ts = time.time()
     h = L.setup(a, ctx=ctx0)
     torch.cuda.synchronize()
-    setup_s = time.time() - ts
+    setup_core_s = time.time() - ts
     if mode == L.MODE_THROUGHPUT:
         L._check(lib.lamg_hier_prepare_throughput(ctx0.p, h.h))
-    log(f"[rank {dist.rank}] setup {setup_s:.2f}s, {h.nlevels} levels")
+    torch.cuda.synchronize()
+    setup_s = time.time() - ts  # hierarchy + THROUGHPUT colouring / inverse / item tables
+    log(f"[rank {dist.rank}] setup {setup_s:.2f}s ({setup_core_s:.2f}s hierarchy), {h.nlevels} levels")
+    relax_levels = [l for l in range(h.nlevels) if h.levels[l].coarsest == 2]
     lanes = [Lane(L, torch, dev, h, mode, B[i * KB:(i + 1) * KB], X0[i * KB:(i + 1) * KB]) for i in range(NL)]
     single = Lane(L, torch, dev, h, mode, b[None], x0[None])
     stream0 = lanes[0].stream
@@ -298,7 +371,7 @@ def run_lamg(args, dist: Dist):
     torch.cuda.synchronize()
     clocks.start()
     launches0 = lib.lamg_launch_count()
-    step_ms, units = [], 0.0
+    step_ms, units, sweeps_units, rhs_done = [], 0.0, 0.0, 0
     all_cycles = []
     # the timed steps are the profiled range (`ncu --profile-from-start off`
     # sees them only; a no-op without a profiler)
@@ -309,6 +382,8 @@ def run_lamg(args, dist: Dist):
         ms, cyc = run_lanes(lanes, Lane.solve_dev, torch, stream0)
         step_ms.append(ms)
         units += float(sum(cyc)) * a.m
+        sweeps_units += float(sum(ln.sweeps_total() for ln in lanes)) * (h.levels[relax_levels[0]].m if relax_levels else 0)
+        rhs_done += nrhs
         all_cycles.append(cyc)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
@@ -319,6 +394,8 @@ def run_lamg(args, dist: Dist):
     max_ms = dist.allreduce(local_ms, "MAX")
     tot_units = dist.allreduce(units, "SUM")
     value = tot_units / (max_ms / 1e3)
+    rhs_per_s = dist.allreduce(float(rhs_done), "SUM") / (max_ms / 1e3)
+    sweeps_per_s = dist.allreduce(sweeps_units, "SUM") / (max_ms / 1e3)
 
     dom = "gs_finest_block" if "gs_finest_block" in kern else ("gs_finest_exact_order" if "gs_finest_exact_order" in kern else None)
     traffic = None
@@ -345,7 +422,8 @@ def run_lamg(args, dist: Dist):
 
     # end to end through the public C-ABI with host (pinned) buffers
     e2e_ms, e2e_units = 0.0, 0.0
-    for i in range(1 + args.steps):  # the device arm already warmed every lane up
+    e2e_steps = max(1, min(args.steps, 3))  # bounded: the device arm already measured the steady state
+    for i in range(1 + e2e_steps):  # the device arm already warmed every lane up
         with torch.cuda.stream(stream0):
             flush.fill_(1.0)
         ms, cyc = run_lanes(lanes, Lane.solve_host, torch, stream0)
@@ -357,7 +435,9 @@ def run_lamg(args, dist: Dist):
     e2e_value = e2e_units / (e2e_max / 1e3)
 
     extra = {}
-    if dist.rank == 0 and not args.skip_validate:
+    # VALIDATE (exact-order everywhere) on the power-law configs' 8-17M-row
+    # relaxation levels takes minutes of wavefront sweeps: only when asked
+    if dist.rank == 0 and not args.skip_validate and (args.config <= 3 or args.validate_big):
         single.solve_host()
         xt, ct = single.x.copy(), single.cycles[0]
         xb = lanes[0].x.copy()  # column 0 of the block (same b and x0)
@@ -366,7 +446,8 @@ def run_lamg(args, dist: Dist):
         xv, sv = L.solve(h, b, x0, L.CycleConfig(), ctx=ctx0)
         extra["validate_mode"] = {"cycles": sv.cycles, "solve_s": round(time.time() - tv, 3), "x_sha": sha(xv)}
         gl = os.path.join(ROOT, "tests", "golden", "large.json")
-        key = {1: "cfg1_grid5_256", 2: "cfg2_grid3d_128"}.get(args.config)
+        key = {1: "cfg1_grid5_256", 2: "cfg2_grid3d_128", 3: "cfg3_rgg_4M", 4: "cfg4_chunglu_16M",
+               5: "cfg5_rmat_25"}.get(args.config)
         if os.path.exists(gl) and key in json.load(open(gl)):
             g = json.load(open(gl))[key]
             if g["b_sha"] == sha(b) and g["x0_sha"] == sha(x0):
@@ -380,7 +461,11 @@ def run_lamg(args, dist: Dist):
 
     out = None
     if dist.rank == 0:
-        cpu = None if args.no_cpu_baseline or dist.world > 1 else cpu_baseline(a, b, x0, args)
+        if args.config >= 4 and not args.validate_big:
+            cpu = {"value": None, "skipped": "a reference setup of this operator takes minutes (BASELINE.md: "
+                                             "~4 min for config 4); run bench.py --impl reference --config N"}
+        else:
+            cpu = None if args.no_cpu_baseline or dist.world > 1 else cpu_baseline(ha, b, x0, args)
         cyc0 = all_cycles[0]
         out = {
             "metric": "fine-level edges*cycles/s (solve to relative residual 1e-10)",
@@ -388,24 +473,30 @@ def run_lamg(args, dist: Dist):
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded generator for BASELINE.json config %d (no dataset involved)" % args.config,
+            "rhs_solved_per_s": rhs_per_s,
             "config": {"workload": WORKLOADS[args.config], "n": a.n, "m": a.m, "mode": args.mode,
-                       "rhs_per_step_per_gpu": nrhs,
+                       "rhs_per_step_per_gpu": nrhs, "lanes": NL, "block": KB,
                        "batching": f"{NL} concurrent lanes (one context/stream each) x a block of {KB} right-hand "
                                    "sides per lane through lamg_solve_batch_dev (node-major n x K vectors, one "
                                    "kernel schedule per block, each column returned at its own convergence); "
                                    "the reference arm runs one solve per host thread",
                        "levels": h.nlevels, "cycles_per_solve": {"min": min(cyc0), "max": max(cyc0),
                                                                  "mean": round(float(np.mean(cyc0)), 2)},
-                       "setup_s": round(setup_s, 3),
+                       "setup_s": round(setup_s, 3), "setup_hierarchy_s": round(setup_core_s, 3),
+                       "operator_build_s": round(gen_s, 2),
+                       "operator_built_on": "device" if args.config >= 4 else "host (numpy, graphs.py)",
                        "single_rhs_solve_ms": round(single_ms, 2), "single_rhs_cycles": single_cycles,
                        "single_rhs_value": a.m * single_cycles / (single_ms / 1e3),
-                       "l2": "L2 flushed (256 MB write) between timed steps; finest operator 183 MB > 126 MB L2",
-                       "parallelism": f"replicas x{dist.world} (each GPU its own right-hand sides, no collective)"},
+                       "l2": "L2 flushed (256 MB write) between timed steps; the finest operator and the "
+                             "K-column vectors exceed the 126 MB L2",
+                       "parallelism": f"replicas x{dist.world} (each GPU its own right-hand sides, no collective)",
+                       "host_cpu": cpu_info()},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "edges*cycles/s", "h2d_bytes_per_step": 16 * a.n * nrhs,
                     "d2h_bytes_per_step": nrhs * (8 * a.n + 8 * (max(cyc0) + 1))},
             "gpu_launches": int(launches),
+            "relaxation_coarsest": relax_info(h, relax_levels, sweeps_per_s, hbm, KB),
             "clocks": clk,
         }
         out.update(extra)
@@ -434,7 +525,7 @@ def cpu_baseline(a, b, x0, args):
     cyc = args.cpu_cycles
     secs, c = h.solve_batch(b[None, :], x0[None, :], 1, max_cycles=cyc)
     v = a.m * float(c[0]) / secs
-    return {"value": v, "unit": "edges*cycles/s", "cores": 1, "kind": kind,
+    return {"value": v, "unit": "edges*cycles/s", "cores": 1, "kind": kind, "host_cpu": cpu_info(),
             "sample": f"{int(c[0])} cycles of one reference solve (max_cycles={cyc}) on the same operator, b and x0; "
                       f"reference setup {setup_s:.1f}s untimed", "setup_s": round(setup_s, 2)}
 
@@ -442,15 +533,18 @@ def cpu_baseline(a, b, x0, args):
 def run_reference(args, dist: Dist):
     if dist.rank != 0:
         return None
-    a, b, x0 = build_inputs(args.config, 0)
+    from paper_1108_1310_b200 import graphs as G
+    a = build_operator(args.config)
     o, kind = _ref_oracle()
     t = time.time()
     h = o.setup(a)
     setup_s = time.time() - t
     threads = os.cpu_count() or 1
-    from paper_1108_1310_b200 import graphs as G
-    B = np.stack([G.gaussian_rhs(a.n, 100 + args.config + 1000 * i) for i in range(threads)])
-    X0 = np.stack([G.default_x0(a.n, seed=1 + i) for i in range(threads)])
+    # the GPU arm's first right-hand sides (rank 0, lanes in order)
+    B = np.stack([G.gaussian_rhs(a.n, rhs_seed(args.config, 0, i)) for i in range(threads)])
+    X0 = np.stack([G.default_x0(a.n, seed=x0_seed(0, i)) for i in range(threads)])
+    if args.config >= 4:
+        B = zero_sum(B)
     cyc = args.cpu_cycles
     for _ in range(args.warmup):
         h.solve_batch(B[:1], X0[:1], 1, max_cycles=1)
@@ -465,12 +559,29 @@ def run_reference(args, dist: Dist):
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic: seeded generator for BASELINE.json config %d" % args.config,
             "config": {"workload": WORKLOADS[args.config], "n": a.n, "m": a.m, "reference_setup_s": round(setup_s, 2),
-                       "parallelism": f"{threads} host threads, one reference solve each"},
+                       "parallelism": f"{threads} host threads, one reference solve each",
+                       "rhs": "the GPU arm's right-hand sides 0..threads-1 of rank 0 (same seeds)",
+                       "host_cpu": cpu_info()},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "edges*cycles/s", "cores": threads, "kind": kind,
                              "sample": f"per step {threads} concurrent reference solves x {cyc} cycles over one "
                                        f"const hierarchy (solve is reentrant, SPEC.md:500)"},
             "e2e": {"value": v, "unit": "edges*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def launch(n: int) -> int:
+    """One process per GPU: re-run this command under torch.distributed.run
+    (single node, 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -482,11 +593,16 @@ def main():
     ap.add_argument("--mode", choices=["throughput", "validate"], default="throughput")
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-cycles", type=int, default=3)
-    ap.add_argument("--lanes", type=int, default=8, help="concurrent solve lanes (contexts/streams) per GPU")
-    ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..32; 1 = single solves)")
+    ap.add_argument("--lanes", type=int, default=0,
+                    help="concurrent solve lanes (contexts/streams) per GPU (0: 8, configs 4/5: 2)")
+    ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..128; 1 = single solves)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")
+    ap.add_argument("--validate-big", action="store_true",
+                    help="configs 4/5: also run the VALIDATE solve and the CPU baseline (minutes)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch(args.gpus))
     dist = Dist(want_gpu=args.impl == "lamg")
     out = run_reference(args, dist) if args.impl == "reference" else run_lamg(args, dist)
     if out is not None:

@@ -36,6 +36,11 @@ CASES = {
     "cfg3s_rgg_256k": (lambda: G.rgg(1 << 18, seed=3), 103),
     "cfg4s_chunglu_256k": (lambda: G.chung_lu(1 << 18, seed=4), 104),
     "cfg5s_rmat_16": (lambda: G.rmat(16, seed=5), 105),
+    # full BASELINE.json sizes (configs 3-5; the GPU tests generate 4 and 5 on
+    # the device and check the input digests against these)
+    "cfg3_rgg_4M": (lambda: G.make_config(3), 103),
+    "cfg4_chunglu_16M": (lambda: G.make_config(4), 104),
+    "cfg5_rmat_25": (lambda: G.make_config(5), 105),
 }
 
 

@@ -79,3 +79,25 @@ def test_two_rank_gloo_sharded_solve():
     single = sum(a.m * float(h.solve(G.gaussian_rhs(a.n, 10 + i), G.default_x0(a.n, seed=1 + i))[1]["cycles"][0])
                  for i in range(5))
     assert tots.pop() == single
+
+
+def test_bench_launcher_two_ranks():
+    """bench.py --gpus 2 without WORLD_SIZE relaunches itself under
+    torch.distributed.run (two ranks, gloo here: the reference arm needs no
+    GPU); rank 0 alone prints the JSON line, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not os.path.exists(os.path.join(root, "oracle", "_ref", "liblamg_ref.so")) and \
+            not os.path.exists(os.path.join(root, "oracle", "liblamg_oracle.so")):
+        pytest.skip("oracle not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "1", "--steps", "1", "--warmup", "0", "--cpu-cycles", "1"],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    out = json.loads(lines[0])
+    assert out["impl"] == "reference" and out["n_gpus"] == 2 and out["value"] > 0
