@@ -5,7 +5,7 @@
  * (setup: elimination, test vectors, affinity, aggregation, Galerkin; solve:
  * residual, Gauss-Seidel, transfers, energy-corrected cycle) as hand-written
  * sm_100a CUDA. The reference has no plugin/FFI layer: its boundary is the
- * C++ API in /root/reference/proj/core/include/lamg/*.hpp. Each entry point
+ * C++ API in /root/reference/proj/core/include/lamg/ (*.hpp). Each entry point
  * below names the reference interface it replaces; include/lamg_b200/lamg.hpp
  * re-exposes them with the reference's exact C++ signatures.
  *

@@ -13,19 +13,25 @@
 // exception types with the reference's message text. The default execution
 // mode is VALIDATE (bit-identical to the reference); lamg::b200::set_mode
 // selects THROUGHPUT (coloured Gauss-Seidel smoother, same hierarchy).
-// Header-only: include it and link -llamg_b200.
+// The hierarchy stays in HBM: Level::op, Level::transfer and
+// Level::coarsest_solver are views whose arrays are downloaded on first use
+// (n, m and every scalar are known at once), so setup() moves no operator to
+// the host. Header-only: include it and link -llamg_b200.
 #pragma once
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "lamg_b200.h"
@@ -73,14 +79,105 @@ struct SetupOptions {
   int tv_count_max = 10;
 };
 
+namespace b200 {
+// A device array of the hierarchy, downloaded (once, thread-safely) on first
+// use; reads like the reference's std::vector member it stands in for.
+template <class T>
+class LazyArray {
+ public:
+  LazyArray() = default;
+  explicit LazyArray(std::function<const std::vector<T>&()> get) : get_(std::move(get)) {}
+  const std::vector<T>& vec() const { return get_ ? get_() : own_; }
+  operator const std::vector<T>&() const { return vec(); }
+  const T& operator[](std::size_t i) const { return vec()[i]; }
+  std::size_t size() const { return vec().size(); }
+  bool empty() const { return vec().empty(); }
+  const T* data() const { return vec().data(); }
+  auto begin() const { return vec().begin(); }
+  auto end() const { return vec().end(); }
+  bool operator==(const std::vector<T>& o) const { return vec() == o; }
+
+ private:
+  std::function<const std::vector<T>&()> get_;
+  std::vector<T> own_;
+};
+
+// a group of arrays filled by one download
+template <class D>
+struct Lazy {
+  std::once_flag once;
+  std::function<void(D&)> load;
+  D data;
+  const D& get() {
+    std::call_once(once, [this] { load(data); });
+    return data;
+  }
+};
+}  // namespace b200
+
+// Level::op: sparse_laplacian.hpp's fields, arrays fetched from HBM on first use
+struct LevelOperator {
+  Index n = 0;
+  EntryCount m = 0;
+  b200::LazyArray<EntryCount> row_ptr;
+  b200::LazyArray<Index> col;
+  b200::LazyArray<Real> val;
+  b200::LazyArray<Real> diag;
+  std::shared_ptr<b200::Lazy<SparseLaplacian>> src;
+  Index degree(Index u) const { return static_cast<Index>(row_ptr[u + 1] - row_ptr[u]); }
+  const SparseLaplacian& laplacian() const { return src->get(); }
+  operator const SparseLaplacian&() const { return laplacian(); }
+};
+
+// elimination.hpp:16-31
+struct ElimStage {
+  Index parent_n = 0;
+  Index coarse_n = 0;
+  b200::LazyArray<Index> f_nodes;
+  b200::LazyArray<Real> f_diag;
+  b200::LazyArray<EntryCount> f_ptr;
+  b200::LazyArray<Index> f_nbr;
+  b200::LazyArray<Real> f_val;
+  b200::LazyArray<Index> coarse_of_parent;
+  b200::LazyArray<Index> parent_of_coarse;
+};
+struct EliminationTransfer {
+  std::vector<ElimStage> stages;
+  LevelOperator coarse_op;  // the eliminated level's operator (the same device arrays as Level::op)
+};
+
+// aggregation.hpp:36-44
+struct AggregationTransfer {
+  Index fine_n = 0;
+  Index coarse_n = 0;
+  b200::LazyArray<Index> aggregate_of;
+  b200::LazyArray<Index> seed_of;
+  int stage_used = 0;
+  double alpha = 1.0;
+  Index dummy_aggregate = -1;
+};
+
+// coarse_solver.hpp:15-24 -- the coarsest-level solvers run on the GPU
+// (direct: bordered LU per component; relaxation: Gauss-Seidel to 1e-12)
+class CoarsestSolver {
+ public:
+  static std::shared_ptr<const CoarsestSolver> make_direct(const SparseLaplacian& a);
+  static std::shared_ptr<const CoarsestSolver> make_relaxation(const SparseLaplacian& a);
+  virtual ~CoarsestSolver() = default;
+  virtual void solve(std::span<const Real> b, std::span<Real> x) const = 0;
+};
+
+// hierarchy.hpp:24-37
 struct Level {
   LevelKind kind = LevelKind::Finest;
-  SparseLaplacian op;  // downloaded from the device hierarchy
+  LevelOperator op;  // device-resident; arrays downloaded on first use
+  std::variant<std::monostate, EliminationTransfer, AggregationTransfer> transfer;
   double gamma = 1.0;
   int nu_pre = 0;
   int nu_post = 0;
   int tv_count = 0;
   CoarsestMode coarsest = CoarsestMode::None;
+  std::shared_ptr<const CoarsestSolver> coarsest_solver;
   bool is_elimination() const { return kind == LevelKind::Elimination; }
   bool is_aggregation() const { return kind == LevelKind::Aggregation; }
 };
@@ -172,7 +269,7 @@ inline lamg_ctx* context() {
   };
   static thread_local Holder h;
   if (!h.p) {
-    if (int rc = lamg_ctx_create(0, mode_ref(), &h.p)) throw Error(lamg_last_error());
+    if (lamg_ctx_create(0, mode_ref(), &h.p) != LAMG_OK) throw Error(lamg_last_error());
   }
   return h.p;
 }
@@ -180,7 +277,7 @@ inline lamg_ctx* context() {
 // selects VALIDATE (bit-identical to the reference) or THROUGHPUT
 inline void set_mode(int mode) {
   mode_ref() = mode;
-  if (int rc = lamg_ctx_set_mode(context(), mode)) throw Error(lamg_last_error());
+  if (lamg_ctx_set_mode(context(), mode) != LAMG_OK) throw Error(lamg_last_error());
 }
 
 [[noreturn]] inline void raise(int code) {
@@ -206,6 +303,97 @@ inline lamg_csr view(const SparseLaplacian& a) {
 
 }  // namespace b200
 
+namespace b200 {
+inline LevelOperator level_operator(std::shared_ptr<lamg_hier> dev, int32_t l, Index n, EntryCount m) {
+  LevelOperator op;
+  op.n = n;
+  op.m = m;
+  auto src = std::make_shared<Lazy<SparseLaplacian>>();
+  src->load = [dev, l, n, m](SparseLaplacian& a) {
+    a.n = n;
+    a.m = m;
+    a.row_ptr.resize(static_cast<std::size_t>(n) + 1);
+    a.col.resize(static_cast<std::size_t>(2 * m));
+    a.val.resize(static_cast<std::size_t>(2 * m));
+    a.diag.resize(static_cast<std::size_t>(n));
+    check(lamg_hier_download_op(dev.get(), l, a.row_ptr.data(), a.col.data(), a.val.data(), a.diag.data()));
+  };
+  op.src = src;
+  op.row_ptr = LazyArray<EntryCount>([src]() -> const std::vector<EntryCount>& { return src->get().row_ptr; });
+  op.col = LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().col; });
+  op.val = LazyArray<Real>([src]() -> const std::vector<Real>& { return src->get().val; });
+  op.diag = LazyArray<Real>([src]() -> const std::vector<Real>& { return src->get().diag; });
+  return op;
+}
+
+inline ElimStage elim_stage(std::shared_ptr<lamg_hier> dev, int32_t l, int32_t s) {
+  ElimStage st;
+  int32_t pn = 0, cn = 0, nf = 0;
+  int64_t nnz = 0;
+  check(lamg_hier_stage_info(dev.get(), l, s, &pn, &cn, &nf, &nnz));
+  st.parent_n = pn;
+  st.coarse_n = cn;
+  struct D {
+    std::vector<Index> f_nodes, f_nbr, cop, poc;
+    std::vector<Real> f_diag, f_val;
+    std::vector<EntryCount> f_ptr;
+  };
+  auto src = std::make_shared<Lazy<D>>();
+  src->load = [dev, l, s, pn, cn, nf, nnz](D& d) {
+    d.f_nodes.resize(nf);
+    d.f_diag.resize(nf);
+    d.f_ptr.resize(static_cast<std::size_t>(nf) + 1);
+    d.f_nbr.resize(static_cast<std::size_t>(nnz));
+    d.f_val.resize(static_cast<std::size_t>(nnz));
+    d.cop.resize(pn);
+    d.poc.resize(cn);
+    check(lamg_hier_download_stage(dev.get(), l, s, d.f_nodes.data(), d.f_diag.data(), d.f_ptr.data(),
+                                   d.f_nbr.data(), d.f_val.data(), d.cop.data(), d.poc.data()));
+  };
+  st.f_nodes = LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().f_nodes; });
+  st.f_diag = LazyArray<Real>([src]() -> const std::vector<Real>& { return src->get().f_diag; });
+  st.f_ptr = LazyArray<EntryCount>([src]() -> const std::vector<EntryCount>& { return src->get().f_ptr; });
+  st.f_nbr = LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().f_nbr; });
+  st.f_val = LazyArray<Real>([src]() -> const std::vector<Real>& { return src->get().f_val; });
+  st.coarse_of_parent = LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().cop; });
+  st.parent_of_coarse = LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().poc; });
+  return st;
+}
+
+// coarse_solver.cpp:26-98 through lamg_k_coarsest_direct / lamg_k_coarsest_relax
+class DeviceCoarsest final : public CoarsestSolver {
+ public:
+  DeviceCoarsest(std::function<const SparseLaplacian&()> op, bool direct) : op_(std::move(op)), direct_(direct) {}
+  void solve(std::span<const Real> b, std::span<Real> x) const override {
+    const SparseLaplacian& a = op_();
+    if (b.size() != static_cast<std::size_t>(a.n) || x.size() != static_cast<std::size_t>(a.n))
+      throw DimensionMismatchError("coarsest solve: vector length does not match the level");
+    const lamg_csr v = view(a);
+    check(direct_ ? lamg_k_coarsest_direct(context(), &v, b.data(), x.data())
+                  : lamg_k_coarsest_relax(context(), &v, b.data(), x.data()));
+  }
+
+ private:
+  std::function<const SparseLaplacian&()> op_;
+  bool direct_;
+};
+
+inline std::shared_ptr<const CoarsestSolver> level_coarsest(const LevelOperator& op, CoarsestMode mode) {
+  auto src = op.src;
+  return std::make_shared<DeviceCoarsest>([src]() -> const SparseLaplacian& { return src->get(); },
+                                          mode == CoarsestMode::Direct);
+}
+}  // namespace b200
+
+inline std::shared_ptr<const CoarsestSolver> CoarsestSolver::make_direct(const SparseLaplacian& a) {
+  auto own = std::make_shared<SparseLaplacian>(a);
+  return std::make_shared<b200::DeviceCoarsest>([own]() -> const SparseLaplacian& { return *own; }, true);
+}
+inline std::shared_ptr<const CoarsestSolver> CoarsestSolver::make_relaxation(const SparseLaplacian& a) {
+  auto own = std::make_shared<SparseLaplacian>(a);
+  return std::make_shared<b200::DeviceCoarsest>([own]() -> const SparseLaplacian& { return *own; }, false);
+}
+
 // hierarchy.hpp:65 -- lamg::setup on the GPU
 inline Hierarchy setup(const SparseLaplacian& a, const SetupOptions& opts = {}) {
   lamg_ctx* ctx = b200::context();
@@ -225,6 +413,7 @@ inline Hierarchy setup(const SparseLaplacian& a, const SetupOptions& opts = {}) 
     b200::check(lamg_hier_warning(raw, i, buf, sizeof buf));
     h.warnings.emplace_back(buf);
   }
+  std::shared_ptr<lamg_hier> dev = h.device;
   for (int32_t l = 0; l < nl; ++l) {
     lamg_level_info li;
     b200::check(lamg_hier_level_info(raw, l, &li));
@@ -235,14 +424,34 @@ inline Hierarchy setup(const SparseLaplacian& a, const SetupOptions& opts = {}) 
     L.nu_post = li.nu_post;
     L.tv_count = li.tv_count;
     L.coarsest = static_cast<CoarsestMode>(li.coarsest);
-    L.op.n = li.n;
-    L.op.m = li.m;
-    L.op.row_ptr.resize(static_cast<size_t>(li.n) + 1);
-    L.op.col.resize(static_cast<size_t>(2 * li.m));
-    L.op.val.resize(static_cast<size_t>(2 * li.m));
-    L.op.diag.resize(static_cast<size_t>(li.n));
-    b200::check(lamg_hier_download_op(raw, l, L.op.row_ptr.data(), L.op.col.data(), L.op.val.data(),
-                                      L.op.diag.data()));
+    L.op = b200::level_operator(dev, l, li.n, li.m);
+    if (L.kind == LevelKind::Aggregation) {
+      AggregationTransfer t;
+      t.fine_n = h.levels.back().op.n;
+      t.coarse_n = li.n;
+      t.stage_used = li.stage_used;
+      t.alpha = li.alpha;
+      t.dummy_aggregate = li.dummy_aggregate;
+      struct Agg {
+        std::vector<Index> aggregate_of, seed_of;
+      };
+      auto src = std::make_shared<b200::Lazy<Agg>>();
+      const Index fn = t.fine_n, cn = li.n;
+      src->load = [dev, l, fn, cn](Agg& d) {
+        d.aggregate_of.resize(static_cast<std::size_t>(fn));
+        d.seed_of.resize(static_cast<std::size_t>(cn));
+        b200::check(lamg_hier_download_agg(dev.get(), l, d.aggregate_of.data(), d.seed_of.data()));
+      };
+      t.aggregate_of = b200::LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().aggregate_of; });
+      t.seed_of = b200::LazyArray<Index>([src]() -> const std::vector<Index>& { return src->get().seed_of; });
+      L.transfer = std::move(t);
+    } else if (L.kind == LevelKind::Elimination) {
+      EliminationTransfer t;
+      for (int32_t s = 0; s < li.nstages; ++s) t.stages.push_back(b200::elim_stage(dev, l, s));
+      t.coarse_op = L.op;
+      L.transfer = std::move(t);
+    }
+    if (L.coarsest != CoarsestMode::None) L.coarsest_solver = b200::level_coarsest(L.op, L.coarsest);
     h.levels.push_back(std::move(L));
   }
   return h;
@@ -311,6 +520,51 @@ inline std::pair<Vector, SolveStats> solve(const Hierarchy& h, std::span<const R
   return {std::move(x), std::move(s)};
 }
 
+// cycle.hpp:61-67 -- residual-minimizing recombination of one or two saved
+// iterates (cycle.cpp:23-103) on the GPU; returns ||b - A y||
+inline Real recombine(const SparseLaplacian& a, std::span<const Real> b, std::span<const Vector> saved_x,
+                      std::span<const Vector> saved_r, std::span<Real> x, Real* before = nullptr) {
+  const auto n = static_cast<std::size_t>(a.n);
+  const std::size_t cols = saved_x.size();
+  if (cols != saved_r.size() || b.size() != n || x.size() != n)
+    throw DimensionMismatchError("recombine: vector lengths do not match the matrix");
+  if (cols == 0) {  // nothing saved: the residual of x itself
+    std::vector<Real> y(n);
+    const lamg_csr v = b200::view(a);
+    b200::check(lamg_k_residual(b200::context(), &v, b.data(), x.data(), y.data()));
+    double s = 0.0;
+    for (double r : y) s += r * r;
+    if (before) *before = std::sqrt(s);
+    return std::sqrt(s);
+  }
+  std::vector<Real> sx(cols * n), sr(cols * n);
+  for (std::size_t i = 0; i < cols; ++i) {
+    if (saved_x[i].size() != n || saved_r[i].size() != n)
+      throw DimensionMismatchError("recombine: vector lengths do not match the matrix");
+    std::copy(saved_x[i].begin(), saved_x[i].end(), sx.begin() + i * n);
+    std::copy(saved_r[i].begin(), saved_r[i].end(), sr.begin() + i * n);
+  }
+  const lamg_csr v = b200::view(a);
+  double bf = 0.0, af = 0.0;
+  b200::check(lamg_k_recombine(b200::context(), &v, b.data(), static_cast<int32_t>(cols), sx.data(), sr.data(),
+                               x.data(), &bf, &af));
+  if (before) *before = bf;
+  return af;
+}
+
+// cycle.hpp:69-74 / cycle.cpp:14-21 (host bookkeeping of the visit schedule)
+struct LevelCredit {
+  std::vector<double> credit;
+  int take(std::size_t level, double gamma) {
+    if (credit.size() <= level) credit.resize(level + 1, 0.0);
+    credit[level] += gamma;
+    int theta = std::max(1, static_cast<int>(std::floor(credit[level])));
+    credit[level] -= theta;
+    if (credit[level] < 0.0) credit[level] = 0.0;
+    return theta;
+  }
+};
+
 // ---- solver.hpp: whole-problem driver (components split on the host, as
 // the reference's L3 driver does; every component is set up and solved on
 // the GPU) --------------------------------------------------------------------
@@ -331,6 +585,13 @@ struct Prepared {
   double setup_work = 0.0;
   double setup_seconds = 0.0;
   std::vector<std::string> warnings;
+  // solver.cpp:23-29: the component with the most nodes (the first on ties)
+  const Hierarchy& largest() const {
+    std::size_t best = 0;
+    for (std::size_t i = 1; i < components.size(); ++i)
+      if (components[i].nodes.size() > components[best].nodes.size()) best = i;
+    return components[best].hierarchy;
+  }
 };
 
 struct SolveReport {
@@ -468,6 +729,25 @@ inline SolveReport solve_prepared(const Prepared& p, std::span<const Real> b, st
   r.solve_work = work_edges / static_cast<double>(std::max<EntryCount>(p.a.m, 1));
   r.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return r;
+}
+
+// solver.hpp:55-63 / solver.cpp:109-118: benchmark measures in finest-MVM
+// equivalents
+struct PerformanceMeasures {
+  double t_setup = 0.0;
+  double t_solve = 0.0;
+  double t_total = 0.0;
+  double setup_fraction = 0.0;
+};
+
+inline PerformanceMeasures performance_measures(double setup_work, double solve_work, double r0, double rp) {
+  PerformanceMeasures m;
+  m.t_setup = setup_work;
+  const double digits = r0 > 0.0 && rp > 0.0 ? std::log10(r0 / rp) : 0.0;
+  m.t_solve = digits > 0.0 ? solve_work / digits : 0.0;
+  m.t_total = m.t_setup + 10.0 * m.t_solve;
+  m.setup_fraction = m.t_total > 0.0 ? m.t_setup / m.t_total : 0.0;
+  return m;
 }
 
 // ------------------------------------------------------- Matrix Market files
