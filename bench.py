@@ -139,12 +139,8 @@ def build_operator(cfg: int, ctx=None):
 
 
 def zero_sum(B):
-    """At n ~ 1e7 the sequential mean subtraction of gaussian_rhs leaves |sum b|
-    near the reference's 1e-10 * max|b| compatibility threshold
-    (cycle.cpp:226-230): project again with a pairwise sum."""
-    for _ in range(2):
-        B -= (B.sum(axis=-1, keepdims=True) / B.shape[-1])
-    return B
+    from paper_1108_1310_b200 import graphs as G
+    return G.zero_sum(B)
 
 
 def cpu_info() -> dict:

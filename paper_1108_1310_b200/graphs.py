@@ -391,6 +391,17 @@ def gaussian_rhs(n: int, seed: int) -> np.ndarray:
     return subtract_mean_seq(z)
 
 
+def zero_sum(B: np.ndarray) -> np.ndarray:
+    """At n ~ 1e7 the sequential mean subtraction of gaussian_rhs leaves |sum b|
+    near the reference's 1e-10 * max|b| compatibility threshold
+    (cycle.cpp:226-230): project again (twice) with numpy's pairwise sum.
+    Used for the full-size configs 4 and 5 by bench.py, the GPU tests and
+    tests/golden/make_golden_large.py alike."""
+    for _ in range(2):
+        B -= (B.sum(axis=-1, keepdims=True) / B.shape[-1])
+    return B
+
+
 def subtract_mean_seq(x: np.ndarray) -> np.ndarray:
     """subtract_mean with the reference's left-to-right fold."""
     s = sequential_sum(x)
@@ -398,11 +409,10 @@ def subtract_mean_seq(x: np.ndarray) -> np.ndarray:
 
 
 def sequential_sum(x: np.ndarray) -> float:
-    """Exact left-to-right fold (numpy's sum is pairwise)."""
-    s = 0.0
-    for v in np.asarray(x, dtype=np.float64).tolist():
-        s += v
-    return s
+    """Exact left-to-right fold (numpy's sum is pairwise; its cumulative sum
+    is the sequential recurrence, so the last prefix is the fold)."""
+    x = np.asarray(x, dtype=np.float64).ravel()
+    return float(np.cumsum(x)[-1]) if x.size else 0.0
 
 
 def default_x0(n: int, seed: int = 1) -> np.ndarray:

@@ -179,12 +179,18 @@ def test_facade_api_matches_oracle(graph, tmp_path):
     assert np.array_equal(_out(d, "x_recomb", np.float64), xr)
     assert int(m["recomb_cycles"]) == int(srr["cycles"][0])
     assert int(m["recomb_recombinations"]) == int(srr["recombinations"][0])
-    with pytest.raises(Exception) as ei:
+    if int(sf["cycles"][0]) == 1:
+        # a one-cycle solve (relaxation coarsest) converges before the divergence
+        # test is reached (cycle.cpp:252-267): neither side throws
         oh.solve(b, x0, divergence_factor=1e-6)
-    assert m["diverged_message"].startswith("solve diverged: residual grew from ")
-    assert m["diverged_message"] in str(ei.value)
-    assert int(m["diverged_cycles"]) == int(ei.value.stats["cycles"][0])
-    assert np.array_equal(_out(d, "res_diverged", np.float64), ei.value.stats["residuals"])
+        assert m["diverged"] == "none"
+    else:
+        with pytest.raises(Exception) as ei:
+            oh.solve(b, x0, divergence_factor=1e-6)
+        assert m["diverged_message"].startswith("solve diverged: residual grew from ")
+        assert m["diverged_message"] in str(ei.value)
+        assert int(m["diverged_cycles"]) == int(ei.value.stats["cycles"][0])
+        assert np.array_equal(_out(d, "res_diverged", np.float64), ei.value.stats["residuals"])
     y, before, after = o.recombine(a, b, sx, sr, rx)
     assert np.array_equal(_out(d, "recombine_x", np.float64), y)
     assert float(m["recombine_before"]) == before and float(m["recombine_after"]) == after

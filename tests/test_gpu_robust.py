@@ -41,7 +41,7 @@ def test_diverged_error_matches_oracle(graph):
     cfg = L.CycleConfig(divergence_factor=1e-6)
     with pytest.raises(L.DivergedError) as ge:
         L.solve(h, b, x0, cfg, ctx=ctx)
-    msg = str(ge.value.args[0])
+    msg = ge.value.msg
     assert msg.startswith("solve diverged: residual grew from ") and msg in str(oe.value)
     st = ge.value.stats
     assert int(st["cycles"][0]) == int(want["cycles"][0]) == 1
@@ -50,7 +50,7 @@ def test_diverged_error_matches_oracle(graph):
     ctx.set_mode(L.MODE_THROUGHPUT)
     with pytest.raises(L.DivergedError) as te:
         L.solve(h, b, x0, cfg, ctx=ctx)
-    assert str(te.value.args[0]).startswith("solve diverged: residual grew from ")
+    assert te.value.msg.startswith("solve diverged: residual grew from ")
     assert int(te.value.stats["cycles"][0]) == 1
     # a block: every column diverges at cycle 1 and reports its own stats
     B = np.stack([b, G.gaussian_rhs(a.n, 18)])
