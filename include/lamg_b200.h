@@ -245,17 +245,25 @@ int lamg_part_plan(const lamg_csr *a, const int32_t *bounds, int32_t nparts, int
  * any) must outlive the partition. */
 int lamg_part_level_create(lamg_ctx *ctx, const lamg_csr *a, const int32_t *bounds, int32_t nparts,
                            int32_t first_part, int32_t nown, lamg_comm *comm, lamg_part_level **out);
-/* the finest level of a hierarchy, partitioned (bounds by lamg_part_bounds) */
+/* the first smoothing level of a hierarchy, partitioned (bounds by
+ * lamg_part_bounds): level 0 when its child is an aggregation level, level 1
+ * when the finest level is reduced by elimination first (cycle.cpp:131-164);
+ * lamg_part_level_n gives its size */
 int lamg_part_level_from_hier(lamg_ctx *ctx, const lamg_hier *h, int32_t nparts, int32_t first_part,
                               int32_t nown, lamg_comm *comm, lamg_part_level **out);
 void lamg_part_level_destroy(lamg_part_level *pl);
-/* lamg_solve with the finest level partitioned (THROUGHPUT, flat cycle, finest
- * level with an aggregation child): finest sweeps/residuals on the parts, the
- * residual allgathered, coarse levels replicated on every rank; bit-identical
- * to lamg_solve on a context with lamg_ctx_set_exact_levels(ctx, 0) (the parts
- * sweep coloured). pl must have been built on ctx (and, from a hierarchy, from
- * h): LAMG_E_ARGUMENT otherwise. b, x0, x: full host vectors (every rank
- * passes all of b). */
+int32_t lamg_part_level_n(const lamg_part_level *pl);
+/* lamg_solve with that level partitioned (THROUGHPUT, flat cycle): its
+ * sweeps/residuals run on the parts, its residual is allgathered, the levels
+ * below are replicated on every rank, and a finest level above it does its
+ * RHS coarsening / injection / back-substitution replicated. A partitioned
+ * relaxation-coarsest level (coarse_solver.cpp:82-93; configs 4 and 5) relaxes
+ * on the parts. With an aggregation child the result is bit-identical to
+ * lamg_solve on a context with lamg_ctx_set_exact_levels(ctx, 0) (the parts
+ * sweep coloured); the relaxation form is bit-identical across part counts
+ * and within rounding of lamg_solve. pl must have been built on ctx (and,
+ * from a hierarchy, from h): LAMG_E_ARGUMENT otherwise. b, x0, x: full host
+ * vectors of the finest level (every rank passes all of b). */
 int lamg_part_solve(lamg_ctx *ctx, const lamg_hier *h, lamg_part_level *pl, const double *b, const double *x0,
                     const lamg_cycle_cfg *cfg, double *x, lamg_solve_stats *stats, double *residuals,
                     int32_t cap);

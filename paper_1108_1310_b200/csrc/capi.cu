@@ -1197,6 +1197,8 @@ void lamg_part_level_destroy(lamg_part_level* pl) {
   delete pl;
 }
 
+int32_t lamg_part_level_n(const lamg_part_level* pl) { return pl ? pl->n : 0; }
+
 int lamg_part_level_from_hier(lamg_ctx* ctx, const lamg_hier* hier, int32_t nparts, int32_t first_part,
                               int32_t nown, lamg_comm* comm, lamg_part_level** out) {
   *out = nullptr;
@@ -1204,7 +1206,7 @@ int lamg_part_level_from_hier(lamg_ctx* ctx, const lamg_hier* hier, int32_t npar
     if (!ctx || !hier || !hier->h) throw LamgError(LAMG_E_ARGUMENT, "null context or hierarchy");
     Ctx& c = ctx->c;
     set_device(c);
-    const DCSR& op = hier->h->levels[0]->op;
+    const DCSR& op = hier->h->levels[part_level_of(*hier->h)]->op;
     std::vector<int64_t> rp = op.rp.to_host();
     std::vector<int32_t> col(2 * op.m);
     std::vector<double> val(2 * op.m), diag(op.n);

@@ -63,14 +63,20 @@ struct PartLevel {
   void interpolate(const int32_t* aggregate_of_full, const double* xc);
 };
 
-// lamg::solve (cycle.cpp:221-273) with the finest level partitioned: the
-// finest sweeps and residuals run on the parts (halo exchange), the finest
-// residual is allgathered so every rank restricts it and runs the coarse
-// levels exactly as one device does (replicated, deterministic). THROUGHPUT,
-// flat cycle, finest level with an aggregation child. Bit-identical to
-// solve_device on one device.
+// lamg::solve (cycle.cpp:221-273) with the first smoothing level partitioned
+// (part_level_of): its sweeps and residuals run on the parts (halo exchange),
+// its residual is allgathered so every rank restricts it and runs the coarse
+// levels exactly as one device does (replicated, deterministic); a
+// relaxation-coarsest level (coarse_solver.cpp:82-93) relaxes on the parts.
+// THROUGHPUT, flat cycle. With an aggregation child the result is
+// bit-identical to solve_device with exact_levels = 0; the relaxation form is
+// bit-identical across part counts.
 struct SolveResult;
 struct CycleCfg;
+struct DHier;
+// the level lamg_part_solve partitions: the finest level that smooths (0, or 1
+// when the finest level is reduced by elimination first)
+int part_level_of(const DHier& h);
 int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, const double* x0, const CycleCfg& cfg,
                       double* x, SolveResult& res);
 

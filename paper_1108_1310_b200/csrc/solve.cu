@@ -815,6 +815,18 @@ int solve_batch_device(Ctx& c, const DHier& h, int nrhs, const double* B, const 
 // correction are exactly the single-device ones on every rank; the
 // interpolation lands on the owned rows. Every kernel and fold order matches
 // solve_device, so the result is bit-identical to it.
+// The partitioned level lp is the finest level that smooths: level 0 when its
+// child is an aggregation level (3D grids), level 1 when level 0 is reduced
+// by elimination first (2D grids, geometric and power-law graphs) -- then the
+// finest level's work is the RHS coarsening (cached, cycle.cpp:139-148), the
+// injection and the back-substitution, replicated on every rank. A level lp
+// that is the relaxation coarsest (configs 4 and 5) runs RelaxationSolver::solve
+// (coarse_solver.cpp:82-93) on the parts: sweep, mean, residual, norm.
+int part_level_of(const DHier& h) {
+  if (h.levels.size() < 2) return 0;
+  return h.levels[1]->kind == KIND_ELIM ? 1 : 0;
+}
+
 int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, const double* x0, const CycleCfg& cfg,
                       double* x, SolveResult& res) {
   const DLevel& L0 = *h.levels[0];
@@ -822,61 +834,136 @@ int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, co
   res = SolveResult{};
   if (c.mode != LAMG_MODE_THROUGHPUT || cfg.correction != 0)
     throw LamgError(LAMG_E_ARGUMENT, "the partitioned solve runs THROUGHPUT mode with the flat cycle");
-  if (h.levels.size() < 2 || h.levels[1]->kind != KIND_AGG)
-    throw LamgError(LAMG_E_ARGUMENT, "the partitioned solve needs a finest level with an aggregation child");
-  if (pl.bounds.back() != n) throw LamgError(LAMG_E_DIMENSION_MISMATCH, "partition does not match the finest level");
+  const int lp = part_level_of(h);
+  const DLevel& LP = *h.levels[lp];
+  const int64_t np = LP.op.n;
+  const bool relax = LP.coarsest == CM_RELAX;
+  if (h.levels.size() < 2 || (!relax && (LP.coarsest != CM_NONE || h.levels[lp + 1]->kind != KIND_AGG)))
+    throw LamgError(LAMG_E_ARGUMENT,
+                    "the partitioned solve needs a smoothing level (aggregation child or relaxation coarsest) at "
+                    "the top of the hierarchy");
+  if (pl.bounds.back() != np)
+    throw LamgError(LAMG_E_DIMENSION_MISMATCH, "partition does not match the hierarchy's first smoothing level");
   check_compatible(c, b, n, false);
   const bool use_tail = prepare_solve(c, h, cfg, false);
   Workspace& ws = *c.ws;
+  ws.top_rhs_valid = false;
   const double w0 = c.work = 0.0;
   double* xw = ws.lv[0].x.p;
   double* bw = ws.lv[0].b.p;
   double* rw = ws.lv[0].r.p;
   copy_d(c, bw, b, n);
   copy_d(c, xw, x0, n);
-  pl.load(bw, xw);
   double* rn_d = c.dscal + 150;
   double* growth = c.dscal + 151;
+  double* rl_d = c.dscal + 152;  // relaxation norms of the partitioned level
   CK(cudaMemsetAsync(growth, 0, sizeof(double), c.s));
   Driver d{c, h, cfg, ws, LevelCredits{}, false, growth};
   d.credits.credit.assign(h.levels.size(), 0.0);
   const double m0 = (double)L0.op.m;
-  auto residual_norm = [&] {
+  const double mp = (double)LP.op.m;
+  // vectors of the partitioned level (level 0's own, or level 1's workspace)
+  double* xp = lp == 0 ? xw : ws.lv[lp].x.p;
+  double* bp = lp == 0 ? bw : ws.lv[lp].b.p;
+  double* rp = ws.lv[lp].r.p;
+  const std::vector<std::unique_ptr<DStage>>* stages = lp == 1 ? &h.levels[1]->stages : nullptr;
+  const size_t S = stages ? stages->size() : 0;
+  std::vector<const double*> rhs(S);
+  if (lp == 1) {  // coarsen the right-hand side once (cycle.cpp:139-148)
+    rhs[0] = bw;
+    for (size_t s = 0; s < S; ++s) {
+      double* out = s + 1 < S ? ws.lv[0].stage_rhs[s + 1].p : bp;
+      coarsen_rhs(c, (*stages)[s]->view(false), rhs[s], out);
+      c.work += (double)(*stages)[s]->nnzf;
+      if (s + 1 < S) rhs[s + 1] = out;
+    }
+  }
+  // one visit of the partitioned level (theta = 1): b in bp, x in xp (full vectors, in and out)
+  auto visit_part = [&] {
+    pl.load(bp, xp);
+    if (relax) {
+      pl.residual();
+      c.work += mp;
+      pl.allgather(true, rp);
+      tree_norm2(c, rp, np, rl_d);
+      const double r0 = read_scalar(c, rl_d);
+      if (r0 == 0.0) return;
+      for (int sweep = 0; sweep < 400; ++sweep) {
+        pl.sweep(1);
+        pl.allgather(false, xp);
+        subtract_mean_tree(c, xp, np);
+        pl.load(nullptr, xp);
+        pl.residual();
+        c.work += 2.0 * mp;
+        pl.allgather(true, rp);
+        tree_norm2(c, rp, np, rl_d);
+        ++d.relax_sweeps;
+        if (read_scalar(c, rl_d) <= 1e-12 * r0) break;
+      }
+      return;
+    }
+    const DLevel& child = *h.levels[lp + 1];
+    const DAgg& t = *child.agg;
+    LevelWS& wc = ws.lv[lp + 1];
+    if (child.nu_pre) {
+      pl.sweep(child.nu_pre);
+      c.work += mp * child.nu_pre;
+    }
     pl.residual();
+    c.work += mp;
+    pl.allgather(true, rp);
+    restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, rp, cfg.mu, wc.b.p);
+    wc.x.zero();
+    const int theta_child = d.credits.take(lp + 1, child.gamma);
+    d.visit(lp + 1, wc.b.p, wc.x.p, theta_child);
+    pl.interpolate(t.aggregate_of.p, wc.x.p);
+    if (child.nu_post) {
+      pl.sweep(child.nu_post);
+      c.work += mp * child.nu_post;
+    }
+    pl.allgather(false, xp);
+  };
+  // r = b - A x on the finest level and its norm: on the parts when they hold
+  // the finest level, replicated otherwise
+  auto residual_norm = [&] {
+    if (lp == 0) {
+      pl.load(nullptr, xw);
+      pl.residual();
+      pl.allgather(true, rw);
+    } else {
+      d.resid(0, bw, xw, rw);
+      c.work -= m0;  // counted below
+    }
     c.work += m0;
-    pl.allgather(true, rw);
     tree_norm2(c, rw, n, rn_d);
   };
+  if (lp == 0) pl.load(bw, xw);
   residual_norm();
   const double r0 = read_scalar(c, rn_d);
   res.residuals.push_back(r0);
-  const DLevel& child = *h.levels[1];
-  const DAgg& t = *child.agg;
-  LevelWS& wc = ws.lv[1];
   if (r0 != 0.0) {
     const double target = r0 / cfg.target_reduction;
     for (int cycle = 1; cycle <= cfg.max_cycles; ++cycle) {
-      // visit(0, b, x, 1): one aggregation visit of the finest level
-      if (child.nu_pre) {
-        pl.sweep(child.nu_pre);
-        c.work += m0 * child.nu_pre;
-      }
-      pl.residual();
-      c.work += m0;
-      pl.allgather(true, rw);
-      restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, rw, cfg.mu, wc.b.p);
-      wc.x.zero();
-      const int theta_child = d.credits.take(1, child.gamma);
-      d.visit(1, wc.b.p, wc.x.p, theta_child);
-      pl.interpolate(t.aggregate_of.p, wc.x.p);
-      if (child.nu_post) {
-        pl.sweep(child.nu_post);
-        c.work += m0 * child.nu_post;
+      if (lp == 0) {
+        visit_part();
+      } else {  // visit_elimination(0) with theta = 1 (cycle.cpp:131-164)
+        const double* cur = xw;
+        for (size_t s = 0; s < S; ++s) {
+          double* out = s + 1 < S ? ws.lv[0].stage_x[s + 1].p : xp;
+          inject(c, (*stages)[s]->view(), cur, out);
+          cur = out;
+        }
+        d.credits.take(1, h.levels[1]->gamma);
+        visit_part();
+        for (size_t s = S; s-- > 0;) {
+          const double* xc = s + 1 < S ? ws.lv[0].stage_x[s + 1].p : xp;
+          double* out = s == 0 ? xw : ws.lv[0].stage_x[s].p;
+          backsub(c, (*stages)[s]->view(), xc, rhs[s], out);
+          c.work += (double)(*stages)[s]->nnzf;
+        }
       }
       // subtract_mean over the whole iterate, then the cycle's residual
-      pl.allgather(false, xw);
       subtract_mean_tree(c, xw, n);
-      pl.load(nullptr, xw);
       residual_norm();
       const double rn = read_scalar(c, rn_d);
       res.residuals.push_back(rn);
@@ -889,7 +976,6 @@ int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, co
         res.acf = std::pow(rn / r0, 1.0 / cycle);
         res.solve_work = (c.work - w0) / m0;
         res.message = "solve diverged: residual grew from " + to_string_f(r0) + " to " + to_string_f(rn);
-        pl.allgather(false, xw);
         copy_d(c, x, xw, n);
         c.sync();
         return LAMG_E_DIVERGED;
@@ -897,13 +983,11 @@ int solve_partitioned(Ctx& c, const DHier& h, PartLevel& pl, const double* b, co
     }
   } else {
     res.converged = true;
-  }
-  if (r0 == 0.0) {
     subtract_mean_tree(c, xw, n);
-  } else {
-    pl.allgather(false, xw);
-    const double rp = res.residuals.back();
-    res.acf = std::pow(rp / r0, 1.0 / (double)res.cycles);
+  }
+  if (r0 != 0.0) {
+    const double rp_ = res.residuals.back();
+    res.acf = std::pow(rp_ / r0, 1.0 / (double)res.cycles);
   }
   copy_d(c, x, xw, n);
   if (use_tail) ws.tail.collect(c, &c.work, &d.relax_sweeps);

@@ -26,12 +26,24 @@ namespace {
 
 constexpr int kTailThreads = 512;
 constexpr int kTailThreadsBatch = 256;
+constexpr int kTailThreadsSlice = 512;
 
+// K-column node-major ops (nm_*): a thread owns one 4-column group of a row.
+// The scope says how work items t map to (row, column group): the cluster
+// and CTA scopes spread a row's K/4 groups over adjacent threads; the slice
+// scope gives each CTA ONE group (its own 4 columns) of every row.
 struct BlockScope {
   __device__ static int64_t tid() { return threadIdx.x; }
   __device__ static int64_t stride() { return blockDim.x; }
   __device__ static void sync() { __syncthreads(); }
   __device__ static bool leader() { return threadIdx.x == 0; }
+  template <int K>
+  __device__ static constexpr int groups() { return K / 4; }
+  __device__ static int k0(int64_t t, int T) { return (int)(t % T) * 4; }
+  template <int K>
+  __device__ static int col0() { return 0; }
+  template <int K>
+  __device__ static constexpr int ncols() { return K; }
 };
 // The tail grid is a single thread-block cluster: its barrier is the
 // hardware cluster barrier (barrier.cluster.arrive.release / wait.acquire),
@@ -41,11 +53,37 @@ struct GridScope {
   __device__ static int64_t stride() { return (int64_t)gridDim.x * blockDim.x; }
   __device__ static void sync() { cg::this_cluster().sync(); }
   __device__ static bool leader() { return blockIdx.x == 0 && threadIdx.x == 0; }
+  template <int K>
+  __device__ static constexpr int groups() { return K / 4; }
+  __device__ static int k0(int64_t t, int T) { return (int)(t % T) * 4; }
+  template <int K>
+  __device__ static int col0() { return 0; }
+  template <int K>
+  __device__ static constexpr int ncols() { return K; }
 };
 
 // K > 1, node-major, one CTA (small levels of the cluster tail: CTA 0 runs
 // them alone, a phase is a __syncthreads instead of a cluster barrier)
 struct CtaScope : BlockScope {};
+
+// K > 1, node-major, column slices: CTA g of K/4 owns columns 4g..4g+3 of
+// every vector of the sub-cycle and runs the whole recursion for them alone
+// (thread per row; a phase is a __syncthreads; no CTA waits on another, and
+// x stays valid in this SM's L1 across phases -- only this CTA writes it)
+__shared__ int g_slice_k0;  // first column of the 4-column slice this CTA is running
+struct SliceScope {
+  __device__ static int64_t tid() { return threadIdx.x; }
+  __device__ static int64_t stride() { return blockDim.x; }
+  __device__ static void sync() { __syncthreads(); }
+  __device__ static bool leader() { return blockIdx.x == 0 && threadIdx.x == 0 && g_slice_k0 == 0; }
+  template <int K>
+  __device__ static constexpr int groups() { return 1; }
+  __device__ static int k0(int64_t, int) { return g_slice_k0; }
+  template <int K>
+  __device__ static int col0() { return g_slice_k0; }
+  template <int K>
+  __device__ static constexpr int ncols() { return 4; }
+};
 
 // ---------------------------------------------------------------- sweeps
 // shared-memory sweep (BlockScope only): every load of the sweep is an LDS
@@ -859,7 +897,7 @@ __device__ inline void nm_gs(const TLevel& L, const double* __restrict__ b, doub
                              const int32_t* done, TailCounters* ctr) {
   __shared__ int32_t s_cp[kMaxColors + 1];
   if (L.ncolors == 0 || sweeps == 0) return;
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   constexpr int U = 8;
   const long long tg = clock64();
   const int nc = L.ncolors;
@@ -869,7 +907,7 @@ __device__ inline void nm_gs(const TLevel& L, const double* __restrict__ b, doub
   __syncthreads();
   const int64_t slot = S::tid() / T;
   const int64_t rstride = S::stride() / T;
-  const int k0 = (int)(S::tid() % T) * kV;
+  const int k0 = S::k0(S::tid(), T);
   bool fz[kV];
   bool any = false;
 #pragma unroll
@@ -965,12 +1003,204 @@ __device__ inline void nm_gs(const TLevel& L, const double* __restrict__ b, doub
   }
 }
 
+// ---------------------------------------------- slice scope, shared memory
+// Small levels of a slice (sl_ok): the CTA's four columns of x live in shared
+// memory for the whole call, and the entries (col, val) of the NEXT colour --
+// a contiguous range of the colour-permuted operator -- stream into a
+// double buffer with cp.async while the current colour is folded from shared
+// memory; each thread's next row (id, extent, diagonal, b) is loaded one phase
+// ahead into registers. A phase then costs shared-memory gathers, the fold in
+// entry order (the arithmetic of nm_gs), a division and a __syncthreads.
+__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// shared memory of one slice call: x and b (32 B per row each), the stored
+// rows' diagonal, extent and natural id, and nb colour buffers of cap entries
+inline int64_t sl_smem_bytes(int64_t n, int64_t cap, int nb) { return 80 * n + 12 * nb * cap + 128; }
+
+// RES = false: `sweeps` coloured Gauss-Seidel sweeps of the slice; RES = true:
+// r = b - A x over the same colour-permuted rows (a row's entries keep their
+// order, so both match nm_gs / nm_residual bit for bit)
+template <int K, bool RES>
+__device__ inline void sl_rows(const TLevel& L, const double* __restrict__ b, double* x, double* r, int sweeps,
+                               const int32_t* done, TailCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int32_t s_cp[kMaxColors + 1], s_e[kMaxColors + 1];
+  const int nc = L.ncolors;
+  if (nc == 0 || sweeps == 0) return;
+  const long long tg = clock64();
+  const int32_t n = L.n;
+  const int64_t cap = L.sl_cap;
+  const int nb = L.sl_nbuf;
+  const int k0 = g_slice_k0;
+  d4* s_x = (d4*)smem;
+  d4* s_b = s_x + n;
+  double* s_val = (double*)(s_b + n);               // [nb][cap]
+  double* s_d = s_val + (int64_t)nb * cap;          // [n]
+  int32_t* s_rp = (int32_t*)(s_d + n);              // [n+1]
+  int32_t* s_id = s_rp + n + 1;                     // [n]
+  int32_t* s_col = s_id + n;                        // [nb][cap]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i <= nc; i += nt) {
+    s_cp[i] = __ldg(L.sl_tab + i);
+    s_e[i] = __ldg(L.sl_tab + nc + 1 + i);
+  }
+  for (int32_t i = tid; i < n; i += nt) {
+    s_x[i] = ld4(x + (int64_t)i * K + k0);
+    s_b[i] = ld4(b + (int64_t)i * K + k0);
+    s_d[i] = __ldg(L.pdiag + i);
+    s_rp[i] = (int32_t)__ldg(L.prp + i);
+    s_id[i] = __ldg(L.row_ids + i);
+  }
+  if (tid == 0) s_rp[n] = (int32_t)__ldg(L.prp + n);
+  bool fz[kV] = {false, false, false, false};
+  bool any = false;
+  if (!RES) {
+#pragma unroll
+    for (int q = 0; q < kV; ++q) {
+      fz[q] = done && done[k0 + q];
+      any = any || fz[q];
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int cc, int buf) {  // the colour's entries -> buffer buf (asynchronous)
+    const int32_t e0 = s_e[cc], e1 = s_e[cc + 1];
+    double* dv = s_val + (int64_t)buf * cap;
+    int32_t* dc = s_col + (int64_t)buf * cap;
+    for (int32_t e = e0 + tid; e < e1; e += nt) {
+      cp_async8(dv + (e - e0), L.pval + e);
+      cp_async4(dc + (e - e0), L.pcol + e);
+    }
+    cp_async_commit();
+  };
+  const int P = sweeps * nc;
+  long long a_stage = clock64() - tg, a_wait = 0, a_issue = 0, a_comp = 0;
+  for (int q = 0; q < nb - 1; ++q) {  // nb - 1 colours in flight ahead of the one being folded
+    if (q < P) issue(q % nc, q % nb);
+    else cp_async_commit();
+  }
+  for (int p = 0; p < P; ++p) {
+    const int cc = p % nc, buf = p % nb;
+    // colour p's entries have landed once at most the nb - 2 newer groups are
+    // pending; the barrier also orders phase p - 1's x writes and frees its buffer
+    const long long t0 = clock64();
+    if (nb == 3) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const long long t1 = clock64();
+    if (p + nb - 1 < P) issue((p + nb - 1) % nc, (p + nb - 1) % nb);
+    else cp_async_commit();
+    const long long t2 = clock64();
+    const double* v = s_val + (int64_t)buf * cap;
+    const int32_t* c = s_col + (int64_t)buf * cap;
+    const int32_t c0 = s_cp[cc], c1 = s_cp[cc + 1], base = s_e[cc];
+    for (int32_t i = c0 + tid; i < c1; i += nt) {
+      const int32_t u = s_id[i];
+      const int32_t r0 = s_rp[i] - base, r1 = s_rp[i + 1] - base;
+      const double d = s_d[i];
+      const d4 bv = s_b[u];
+      double s0, s1, s2, s3;
+      if (RES) {
+        const d4 xu = s_x[u];
+        s0 = d * xu.x, s1 = d * xu.y, s2 = d * xu.z, s3 = d * xu.w;
+      } else {
+        s0 = bv.x, s1 = bv.y, s2 = bv.z, s3 = bv.w;
+      }
+      // entries in batches of U: the batch's (col, val) and x reads are issued
+      // together, then folded in entry order
+      constexpr int U = 8;
+      for (int32_t e0 = r0; e0 < r1; e0 += U) {
+        int32_t cj[U];
+        double w[U];
+        d4 xv[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const bool ok = e0 + j < r1;
+          cj[j] = ok ? c[e0 + j] : 0;
+          w[j] = ok ? v[e0 + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) xv[j] = s_x[cj[j]];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (e0 + j < r1) {
+            if (RES) {
+              s0 = s0 + w[j] * xv[j].x;
+              s1 = s1 + w[j] * xv[j].y;
+              s2 = s2 + w[j] * xv[j].z;
+              s3 = s3 + w[j] * xv[j].w;
+            } else {
+              s0 = s0 - w[j] * xv[j].x;
+              s1 = s1 - w[j] * xv[j].y;
+              s2 = s2 - w[j] * xv[j].z;
+              s3 = s3 - w[j] * xv[j].w;
+            }
+          }
+      }
+      if (RES) {
+        st4(r + (int64_t)u * K + k0, bv.x - s0, bv.y - s1, bv.z - s2, bv.w - s3);
+      } else {
+        d4 o{s0 / d, s1 / d, s2 / d, s3 / d};
+        if (any) {
+          const d4 old = s_x[u];
+          if (fz[0]) o.x = old.x;
+          if (fz[1]) o.y = old.y;
+          if (fz[2]) o.z = old.z;
+          if (fz[3]) o.w = old.w;
+        }
+        s_x[u] = o;
+      }
+    }
+    a_wait += t1 - t0;
+    a_issue += t2 - t1;
+    a_comp += clock64() - t2;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (!RES) {
+    for (int32_t i = tid; i < n; i += nt) {
+      const d4 o = s_x[i];
+      st4(x + (int64_t)i * K + k0, o.x, o.y, o.z, o.w);
+    }
+  }
+  __syncthreads();
+  if (!RES && SliceScope::leader()) {
+    ctr->phases += (long long)P;
+    ctr->smem_calls += 1;
+    ctr->smem_phases += (long long)P;
+    ctr->lvl_gs_cyc[L.id] += clock64() - tg;
+    ctr->lvl_gs_calls[L.id] += 1;
+    ctr->lvl_ph[L.id][0] += a_stage;  // slice sweeps: staging, cp.async wait + barrier, issue, fold
+    ctr->lvl_ph[L.id][1] += a_wait;
+    ctr->lvl_ph[L.id][2] += a_issue;
+    ctr->lvl_ph[L.id][3] += a_comp;
+  }
+}
+template <int K>
+__device__ inline void sl_gs(const TLevel& L, const double* __restrict__ b, double* x, int sweeps,
+                             const int32_t* done, TailCounters* ctr) {
+  sl_rows<K, false>(L, b, x, nullptr, sweeps, done, ctr);
+}
+template <int K>
+__device__ inline void sl_residual(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
+  sl_rows<K, true>(L, b, const_cast<double*>(x), r, 1, nullptr, nullptr);
+}
+
 template <class S, int K>
 __device__ inline void nm_residual(const TLevel& L, const double* __restrict__ b, const double* x, double* r) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)L.n * T; t += S::stride()) {
     const int64_t u = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const double d = __ldg(L.diag + u);
     const d4 xu = ld4(x + u * K + k0);
     double sv[kV] = {d * xu.x, d * xu.y, d * xu.z, d * xu.w};
@@ -983,10 +1213,10 @@ __device__ inline void nm_residual(const TLevel& L, const double* __restrict__ b
 
 template <class S, int K>
 __device__ inline void nm_restrict(const TLevel& L, const TLevel& C, const double* r, double mu) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)C.n * T; t += S::stride()) {
     const int64_t g = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     double sv[kV] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t j = __ldg(L.mem_ptr + g); j < __ldg(L.mem_ptr + g + 1); ++j) {
       const d4 rv = ld4(r + (int64_t)__ldg(L.mem + j) * K + k0);
@@ -1004,10 +1234,10 @@ __device__ inline void nm_restrict(const TLevel& L, const TLevel& C, const doubl
 
 template <class S, int K>
 __device__ inline void nm_interp(const TLevel& L, const TLevel& C, double* x) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)L.n * T; t += S::stride()) {
     const int64_t u = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const d4 xv = ld4(x + u * K + k0);
     const d4 cv = ld4(C.x + (int64_t)__ldg(L.agg + u) * K + k0);
     st4(x + u * K + k0, xv.x + cv.x, xv.y + cv.y, xv.z + cv.z, xv.w + cv.w);
@@ -1017,10 +1247,10 @@ __device__ inline void nm_interp(const TLevel& L, const TLevel& C, double* x) {
 
 template <class S, int K>
 __device__ inline void nm_coarsen(const StageV& s, const double* b, double* bc) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
     const int64_t q = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const d4 bv = ld4(b + (int64_t)__ldg(s.poc + q) * K + k0);
     double v[kV] = {bv.x, bv.y, bv.z, bv.w};
     for (int64_t j = __ldg(s.t_ptr + q); j < __ldg(s.t_ptr + q + 1); ++j) {
@@ -1040,10 +1270,10 @@ __device__ inline void nm_coarsen(const StageV& s, const double* b, double* bc) 
 
 template <class S, int K>
 __device__ inline void nm_inject(const StageV& s, const double* x, double* xc) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
     const int64_t q = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const d4 v = ld4(x + (int64_t)__ldg(s.poc + q) * K + k0);
     st4(xc + q * K + k0, v.x, v.y, v.z, v.w);
   }
@@ -1052,17 +1282,17 @@ __device__ inline void nm_inject(const StageV& s, const double* x, double* xc) {
 
 template <class S, int K>
 __device__ inline void nm_backsub(const StageV& s, const double* xc, const double* b, double* x) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int64_t t = S::tid(); t < (int64_t)s.coarse_n * T; t += S::stride()) {
     const int64_t q = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const d4 v = ld4(xc + q * K + k0);
     st4(x + (int64_t)__ldg(s.poc + q) * K + k0, v.x, v.y, v.z, v.w);
   }
   S::sync();
   for (int64_t t = S::tid(); t < (int64_t)s.nf * T; t += S::stride()) {
     const int64_t i = t / T;
-    const int k0 = (int)(t % T) * kV;
+    const int k0 = S::k0(t, T);
     const int32_t f = __ldg(s.f_nodes + i);
     const d4 bv = ld4(b + (int64_t)f * K + k0);
     double sv[kV] = {bv.x, bv.y, bv.z, bv.w};
@@ -1083,13 +1313,13 @@ __device__ inline void nm_backsub(const StageV& s, const double* xc, const doubl
 // X = Minv[:n,:n] B per component (the throughput inverse; bdirect's order)
 template <class S, int K>
 __device__ inline void nm_direct(const TLevel& L, const double* b, double* x) {
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
   for (int32_t ci = 0; ci < L.ncomp; ++ci) {
     const int32_t s0 = __ldg(L.comp_start + ci), cn = __ldg(L.comp_start + ci + 1) - s0;
     const double* Mi = L.inv + __ldg(L.inv_off + ci);
     for (int64_t t = S::tid(); t < (int64_t)cn * T; t += S::stride()) {
       const int32_t i = (int32_t)(t / T);
-      const int k0 = (int)(t % T) * kV;
+      const int k0 = S::k0(t, T);
       double sv[kV] = {0.0, 0.0, 0.0, 0.0};
       for (int32_t j = 0; j < cn; ++j) {
         const double m = __ldg(Mi + (int64_t)i * cn + j);
@@ -1112,9 +1342,11 @@ template <class S, int K, bool SQ>
 __device__ inline void nm_colsum(const double* X, int64_t n, double* part, double* s_out) {
   const int64_t R = (n + kChunks - 1) / kChunks;
   const int np = (int)((n + R - 1) / R);
-  for (int64_t t = S::tid(); t < (int64_t)np * K; t += S::stride()) {
-    const int64_t p = t / K;
-    const int k = (int)(t % K);
+  constexpr int NC = S::template ncols<K>();  // the columns this scope's CTAs own
+  const int c0 = S::template col0<K>();
+  for (int64_t t = S::tid(); t < (int64_t)np * NC; t += S::stride()) {
+    const int64_t p = t / NC;
+    const int k = c0 + (int)(t % NC);
     const int64_t u1 = (p + 1) * R < n ? (p + 1) * R : n;
     double s = 0.0;
     for (int64_t u = p * R; u < u1; ++u) {
@@ -1124,10 +1356,11 @@ __device__ inline void nm_colsum(const double* X, int64_t n, double* part, doubl
     part[(int64_t)k * kChunks + p] = s;
   }
   S::sync();
-  if ((int)threadIdx.x < K) {
+  if ((int)threadIdx.x < NC) {
+    const int k = c0 + (int)threadIdx.x;
     double tot = 0.0;
-    for (int p = 0; p < np; ++p) tot += ((volatile double*)part)[(int64_t)threadIdx.x * kChunks + p];
-    s_out[threadIdx.x] = tot;
+    for (int p = 0; p < np; ++p) tot += ((volatile double*)part)[(int64_t)k * kChunks + p];
+    s_out[k] = tot;
   }
   S::sync();  // part is reused by the next sum
 }
@@ -1138,25 +1371,33 @@ template <class S, int K>
 __device__ inline void nm_relax(const TLevel& L, const double* b, double* x, double* part, TailCounters* ctr) {
   __shared__ int32_t s_done[kMaxBlock];
   __shared__ double s_r0[kMaxBlock], s_sum[kMaxBlock];
-  constexpr int T = K / kV;
+  constexpr int T = S::template groups<K>();
+  constexpr int NC = S::template ncols<K>();
+  const int c0 = S::template col0<K>();
   const int64_t n = L.n;
   nm_residual<S, K>(L, b, x, L.r);
   nm_colsum<S, K, true>(L.r, n, part, s_sum);
-  if ((int)threadIdx.x < K) {
-    s_r0[threadIdx.x] = sqrt(s_sum[threadIdx.x]);
-    s_done[threadIdx.x] = s_r0[threadIdx.x] == 0.0;
+  if ((int)threadIdx.x < NC) {
+    const int k = c0 + (int)threadIdx.x;
+    s_r0[k] = sqrt(s_sum[k]);
+    s_done[k] = s_r0[k] == 0.0;
   }
   __syncthreads();
   if (S::leader()) ctr->work += (double)L.m;
   for (int sweep = 0; sweep < 400; ++sweep) {
     int active = 0;
-    for (int k = 0; k < K; ++k) active += !s_done[k];
+    for (int k = c0; k < c0 + NC; ++k) active += !s_done[k];
     if (!active) break;
-    nm_gs<S, K>(L, b, x, 1, s_done, ctr);
+    if constexpr (std::is_same<S, SliceScope>::value) {
+      if (L.sl_ok) sl_gs<K>(L, b, x, 1, s_done, ctr);
+      else nm_gs<S, K>(L, b, x, 1, s_done, ctr);
+    } else {
+      nm_gs<S, K>(L, b, x, 1, s_done, ctr);
+    }
     nm_colsum<S, K, false>(x, n, part, s_sum);
     for (int64_t t = S::tid(); t < n * T; t += S::stride()) {
       const int64_t u = t / T;
-      const int k0 = (int)(t % T) * kV;
+      const int k0 = S::k0(t, T);
 #pragma unroll
       for (int q = 0; q < kV; ++q)
         if (!s_done[k0 + q]) x[u * K + k0 + q] -= s_sum[k0 + q] / (double)n;
@@ -1164,12 +1405,16 @@ __device__ inline void nm_relax(const TLevel& L, const double* b, double* x, dou
     S::sync();
     nm_residual<S, K>(L, b, x, L.r);
     nm_colsum<S, K, true>(L.r, n, part, s_sum);
+    // (slice scope: every CTA sweeps until its own columns are done; the
+    // counters follow CTA 0's columns)
     if (S::leader()) {
       ctr->work += 2.0 * (double)L.m;
       ctr->relax_sweeps += 1;
     }
-    if ((int)threadIdx.x < K && !s_done[threadIdx.x] && sqrt(s_sum[threadIdx.x]) <= 1e-12 * s_r0[threadIdx.x])
-      s_done[threadIdx.x] = 1;
+    if ((int)threadIdx.x < NC) {
+      const int k = c0 + (int)threadIdx.x;
+      if (!s_done[k] && sqrt(s_sum[k]) <= 1e-12 * s_r0[k]) s_done[k] = 1;
+    }
     __syncthreads();
   }
 }
@@ -1188,8 +1433,11 @@ __device__ inline void op_gs(const TLevel& L, const double* b, double* x, int sw
     } else {
       nm_gs<GridScope, K>(L, b, x, sweeps, nullptr, ctr);
     }
+  } else if constexpr (std::is_same<S, SliceScope>::value) {
+    if (L.sl_ok) sl_gs<K>(L, b, x, sweeps, nullptr, ctr);
+    else nm_gs<S, K>(L, b, x, sweeps, nullptr, ctr);
   } else if constexpr (std::is_same<S, CtaScope>::value) {
-    nm_gs<CtaScope, K>(L, b, x, sweeps, nullptr, ctr);
+    nm_gs<S, K>(L, b, x, sweeps, nullptr, ctr);
   }
   else if (L.smem_cs) cs_gs_smem<K>(L, b, x, sweeps, ctr);
   else cs_gs<K>(L, b, x, sweeps, nullptr, ctr);
@@ -1197,6 +1445,10 @@ __device__ inline void op_gs(const TLevel& L, const double* b, double* x, int sw
 template <class S, int K>
 __device__ inline void op_residual(const TLevel& L, const double* b, const double* x, double* r) {
   if constexpr (K == 1) residual<S>(L, b, x, r);
+  else if constexpr (std::is_same<S, SliceScope>::value) {
+    if (L.sl_ok) sl_residual<K>(L, b, x, r);
+    else nm_residual<S, K>(L, b, x, r);
+  }
   else if constexpr (!std::is_same<S, BlockScope>::value) nm_residual<S, K>(L, b, x, r);
   else cs_residual<K>(L, b, x, r);
 }
@@ -1248,6 +1500,28 @@ struct Frame {
   int l, theta, it, step;
 };
 
+// per-operation cycle counters of the K-column tails (LAMG_TAIL_DEBUG)
+__device__ inline long long now_cycles() { return clock64(); }
+template <class S>
+struct OpTimer {
+  TailCounters* ctr;
+  int op;
+  long long t0;
+  __device__ OpTimer(TailCounters* c, int o) : ctr(c), op(o), t0(now_cycles()) {}
+  __device__ ~OpTimer() {
+    if (S::leader()) {
+      const int k = op + (std::is_same<S, SliceScope>::value ? 8 : 0);
+      ctr->op_cyc[k] += now_cycles() - t0;
+      ctr->op_calls[k] += 1;
+    }
+  }
+};
+#define OP_TIMED(op, call)     \
+  do {                         \
+    OpTimer<S> tm_(ctr, op);   \
+    call;                      \
+  } while (0)
+
 // LevelCredit::take on the CTA's shared credits
 __device__ inline int take(double* credits, int l, double gamma) {
   double cr = credits[l] + gamma;
@@ -1270,6 +1544,30 @@ template <int K>
 __device__ inline bool small_handoff(const TLevel* levels, const Frame& f, double* credits, double mu,
                                      int32_t small_rows, double* sh, double* part, TailCounters* ctr,
                                      int32_t xs_rows) {
+  if constexpr (K > 1) {
+    // K > 1: subtrees rooted at levels of at most xs_rows rows run as 4-column
+    // slices, one per CTA (two rounds when there are more slices than CTAs):
+    // no barrier between CTAs inside, x in shared memory (sl_gs)
+    if (levels[f.l].n <= xs_rows) {
+      __shared__ double credits0[kMaxLevels];
+      const int nslices = K / kV;
+      if (nslices > (int)gridDim.x) {
+        for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) credits0[l] = credits[l];
+        __syncthreads();
+      }
+      for (int g = blockIdx.x; g < nslices; g += gridDim.x) {
+        if (g != (int)blockIdx.x) {  // a second slice repeats the same visits: same credits
+          __syncthreads();
+          for (int l = threadIdx.x; l < kMaxLevels; l += blockDim.x) credits[l] = credits0[l];
+        }
+        if (threadIdx.x == 0) g_slice_k0 = g * kV;
+        __syncthreads();
+        visit_loop<SliceScope, K>(levels, f.l, f.theta, credits, mu, small_rows, sh, part, ctr, xs_rows);
+      }
+      GridScope::sync();
+      return true;
+    }
+  }
   if (levels[f.l].n > small_rows) return false;
   // K > 1: CTA 0 runs the small subtree for all K columns, node-major
   using Small = typename std::conditional<K == 1, BlockScope, CtaScope>::type;
@@ -1293,7 +1591,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
     }
     const TLevel& L = levels[f.l];
     if (L.coarsest == CM_DIRECT) {
-      op_direct<S, K>(L, L.b, L.x);
+      OP_TIMED(7, (op_direct<S, K>(L, L.b, L.x)));
       if (S::leader()) ctr->work += (double)L.m;
       --sp;
       continue;
@@ -1310,16 +1608,16 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
           --sp;
           continue;
         }
-        if (C.nu_pre) op_gs<S, K>(L, L.b, L.x, C.nu_pre, ctr, xs_rows);
-        op_residual<S, K>(L, L.b, L.x, L.r);
-        op_restrict<S, K>(L, C, L.r, mu);
+        if (C.nu_pre) OP_TIMED(0, (op_gs<S, K>(L, L.b, L.x, C.nu_pre, ctr, xs_rows)));
+        OP_TIMED(1, (op_residual<S, K>(L, L.b, L.x, L.r)));
+        OP_TIMED(2, (op_restrict<S, K>(L, C, L.r, mu)));
         if (S::leader()) ctr->work += (double)L.m * (C.nu_pre + 1);
         const int th = take(credits, f.l + 1, C.gamma);
         f.step = 1;
         st[sp++] = Frame{f.l + 1, th, 0, 0};
       } else {
-        op_interp<S, K>(L, C, L.x);
-        if (C.nu_post) op_gs<S, K>(L, L.b, L.x, C.nu_post, ctr, xs_rows);
+        OP_TIMED(3, (op_interp<S, K>(L, C, L.x)));
+        if (C.nu_post) OP_TIMED(0, (op_gs<S, K>(L, L.b, L.x, C.nu_post, ctr, xs_rows)));
         if (S::leader()) ctr->work += (double)L.m * C.nu_post;
         ++f.it;
         f.step = 0;
@@ -1330,7 +1628,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
           const double* in = L.b;
           for (int s = 0; s < L.nstages; ++s) {
             double* out = s + 1 < L.nstages ? L.stage_rhs[s + 1] : C.b;
-            op_coarsen<S, K>(L.stages[s], in, out);
+            OP_TIMED(4, (op_coarsen<S, K>(L.stages[s], in, out)));
             in = out;
           }
           if (S::leader()) ctr->work += (double)L.elim_nnz;
@@ -1342,7 +1640,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
         const double* cur = L.x;
         for (int s = 0; s < L.nstages; ++s) {
           double* out = s + 1 < L.nstages ? L.stage_x[s + 1] : C.x;
-          op_inject<S, K>(L.stages[s], cur, out);
+          OP_TIMED(5, (op_inject<S, K>(L.stages[s], cur, out)));
           cur = out;
         }
         const int th = take(credits, f.l + 1, C.gamma);
@@ -1353,7 +1651,7 @@ __device__ void visit_loop(const TLevel* __restrict__ levels, int l0, int theta0
           const double* xc = s + 1 < L.nstages ? L.stage_x[s + 1] : C.x;
           double* out = s == 0 ? L.x : L.stage_x[s];
           const double* rhs = s == 0 ? L.b : L.stage_rhs[s];
-          op_backsub<S, K>(L.stages[s], xc, rhs, out);
+          OP_TIMED(6, (op_backsub<S, K>(L.stages[s], xc, rhs, out)));
         }
         if (S::leader()) ctr->work += (double)L.elim_nnz;
         ++f.it;
@@ -1393,7 +1691,8 @@ __global__ void __launch_bounds__(kTailThreadsBatch, 1) subtree_kernel(const TLe
   __shared__ double credits[kMaxLevels];
   __shared__ double sh[64];
   const long long t_start = clock64();
-  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = credits_g[l];
+  double* mine = credits_g + (int64_t)blockIdx.x * kMaxLevels;  // per-CTA copy (see slice_kernel)
+  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = mine[l];
   // the root level arrives node-major from the host-driven levels: my columns in
   const TLevel& R = levels[l0];
   const ColSlice sl = my_cols<K>();
@@ -1409,10 +1708,30 @@ __global__ void __launch_bounds__(kTailThreadsBatch, 1) subtree_kernel(const TLe
     const int64_t u = t >> sl.sh, k = sl.k0 + (t & (sl.kc - 1));
     R.nm_x[u * K + k] = R.x[k * n + u];
   }
-  if (blockIdx.x == 0) {
-    for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits_g[l] = credits[l];
-    if (threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
-  }
+  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) mine[l] = credits[l];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
+}
+
+// K > 1, column slices (the default block tail): K/4 independent CTAs, CTA g
+// the whole sub-cycle for columns 4g..4g+3 on the node-major vectors in place
+// (its 32-byte sector of every row) -- no cluster, no barrier between CTAs
+template <int K>
+__global__ void __launch_bounds__(kTailThreadsSlice, 1) slice_kernel(const TLevel* __restrict__ levels, int nlevels,
+                                                                    int l0, int theta0, double* credits_g, double mu,
+                                                                    int32_t small_rows, double* part,
+                                                                    TailCounters* ctr, int32_t xs_rows) {
+  __shared__ double credits[kMaxLevels];
+  __shared__ double sh[64];
+  const long long t_start = clock64();
+  // every CTA keeps its own copy of the (identical) credits: no CTA reads
+  // what another writes, whenever each is scheduled
+  double* mine = credits_g + (int64_t)blockIdx.x * kMaxLevels;
+  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) credits[l] = mine[l];
+  if (threadIdx.x == 0) g_slice_k0 = (int)blockIdx.x * kV;
+  __syncthreads();
+  visit_loop<SliceScope, K>(levels, l0, theta0, credits, mu, small_rows, sh, part, ctr, xs_rows);
+  for (int l = threadIdx.x; l < nlevels; l += blockDim.x) mine[l] = credits[l];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->cyc_total += clock64() - t_start;
 }
 
 }  // namespace
@@ -1423,6 +1742,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   // LAMG_BATCH_TAIL=subtree selects the per-column CTA subtree below 4096 rows
   const char* et = getenv("LAMG_BATCH_TAIL");
   subtree = ws.K > 1 && ws.K <= 32 && et && strcmp(et, "subtree") == 0;
+  slice = ws.K > 1 && !subtree && et && strcmp(et, "slice") == 0;
   const bool nm = ws.K > 1 && !subtree;
   if (subtree) {
     const char* eb = getenv("LAMG_BATCH_SMALL");
@@ -1525,22 +1845,76 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
     xs_rows = 0;
     smem = std::min(smem, kTailSmemMax);
   }
+  if (nm) {
+    // slice scope (the standalone slice kernel, and the cluster tail's small
+    // subtrees): levels whose x slice and two colour buffers fit the dynamic
+    // shared memory sweep from it (sl_gs); the cluster hands a subtree to the
+    // slices when every level in it does (LAMG_BATCH_SLICE_ROWS caps the root)
+    const int64_t budget = kTailSmemMax;
+    int64_t need = 0;
+    std::vector<int32_t> sl_tab_h;
+    std::vector<int64_t> sl_off(nl, -1);
+    for (int l = first; l < nl; ++l) {
+      const DLevel& L = *h.levels[l];
+      if (!L.color) continue;
+      const std::vector<int64_t> rp = L.color->rp.to_host();
+      int64_t cap = 0;
+      for (int32_t cc = 0; cc < L.color->ncolors; ++cc)
+        cap = std::max(cap, rp[L.color->cptr_h[cc + 1]] - rp[L.color->cptr_h[cc]]);
+      cap = (cap + 1) / 2 * 2;
+      tl[l].sl_cap = (int32_t)cap;
+      sl_off[l] = (int64_t)sl_tab_h.size();
+      for (int32_t cc = 0; cc <= L.color->ncolors; ++cc) sl_tab_h.push_back(L.color->cptr_h[cc]);
+      for (int32_t cc = 0; cc <= L.color->ncolors; ++cc) sl_tab_h.push_back((int32_t)rp[L.color->cptr_h[cc]]);
+      tl[l].sl_nbuf = sl_smem_bytes(L.op.n, cap, 3) <= budget ? 3 : 2;
+      tl[l].sl_ok = L.color->ncolors <= kMaxColors && 2 * L.op.m < (1ll << 31) &&
+                    sl_smem_bytes(L.op.n, cap, tl[l].sl_nbuf) <= budget;
+      if (tl[l].sl_ok) need = std::max(need, sl_smem_bytes(L.op.n, cap, tl[l].sl_nbuf));
+    }
+    sl_tabs.alloc(std::max<int64_t>((int64_t)sl_tab_h.size(), 1), c.s);
+    sl_tabs.upload(sl_tab_h.data(), (int64_t)sl_tab_h.size());
+    for (int l = first; l < nl; ++l) tl[l].sl_tab = sl_off[l] >= 0 ? sl_tabs.p + sl_off[l] : nullptr;
+    const char* er = getenv("LAMG_BATCH_SLICE_ROWS");
+    const int32_t cap_rows = er ? atoi(er) : 1 << 30;
+    int root = nl;  // first level of the all-sl_ok suffix
+    for (int l = nl - 1; l >= first; --l) {
+      const DLevel& L = *h.levels[l];
+      const bool ok = (!L.color || tl[l].sl_ok) && L.op.n <= cap_rows && L.coarsest != CM_RELAX;
+      if (!ok) break;
+      root = l;
+    }
+    xs_rows = !slice && root < nl ? h.levels[root]->op.n : 0;
+    if (!slice && root >= nl) need = 0;
+    smem = (int)need;
+  }
   K = ws.K;
   if (subtree) {  // column-slice sweeps stage operator + slice in shared memory
     const char* e6 = getenv("LAMG_BATCH_SMEM_KB");
     smem = std::min(kTailSmemMax, (e6 ? atoi(e6) : 200) * 1024);
   }
-  credits.alloc(nl, c.s);
+  credits.alloc((int64_t)kMaxLevels * (kMaxBlock / kV), c.s);  // a slot per CTA of the slice / subtree forms
   ctr.alloc(1, c.s);
   const char* e4 = getenv("LAMG_TAIL_OCC");
   occ2 = !(e4 && atoi(e4) == 1);
-  threads = K > 1 ? kTailThreadsBatch : kTailThreads;
+  threads = K > 1 ? (slice ? kTailThreadsSlice : kTailThreadsBatch) : kTailThreads;
+  if (slice) ctas = K / kV;
   if (subtree) {
     const char* ek = getenv("LAMG_BATCH_KC");
     int kc = ek ? std::max(1, atoi(ek)) : 1;
     while (K % kc) --kc;
     ctas = K / kc;
   }
+  if (slice) {
+    switch (K) {
+      case 4: kernel = (const void*)slice_kernel<4>; break;
+      case 8: kernel = (const void*)slice_kernel<8>; break;
+      case 16: kernel = (const void*)slice_kernel<16>; break;
+      case 32: kernel = (const void*)slice_kernel<32>; break;
+      case 64: kernel = (const void*)slice_kernel<64>; break;
+      case 128: kernel = (const void*)slice_kernel<128>; break;
+      default: throw LamgError(LAMG_E_ARGUMENT, "tail: unsupported batch width");
+    }
+  } else
   switch (K) {
     case 1: kernel = occ2 ? (const void*)tail_kernel<2, 1> : (const void*)tail_kernel<1, 1>; break;
     // K > 1: 256 threads (255 registers) -- the column-slice phases are
@@ -1560,7 +1934,7 @@ void TailPlan::build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows) {
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax));
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   // largest cluster the device can co-schedule with this footprint
-  while (!subtree && ctas > 1) {
+  while (!subtree && !slice && ctas > 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
     cfg.blockDim = dim3(threads);
@@ -1628,7 +2002,7 @@ void TailPlan::run(Ctx& c, int l, int theta, double mu, int nlevels) {
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
-  cfg.numAttrs = subtree ? 0 : 1;
+  cfg.numAttrs = subtree || slice ? 0 : 1;
   count_launch();
   int32_t xr = xs_rows;
   void* args[] = {(void*)&lv, &nlevels, &l, &theta, &cr, &mu, &sr, &pt, &ct, &xr};
@@ -1658,6 +2032,12 @@ void TailPlan::print_debug(const TailCounters& h) const {
     fprintf(stderr, "[tail] grid phase breakdown (CTA0 thread0, cycles/phase): fold %.0f extra %.0f prefetch %.0f barrier %.0f\n",
             (double)h.ph_fold / h.global_phases, (double)h.ph_extra / h.global_phases,
             (double)h.ph_prefetch / h.global_phases, (double)h.ph_barrier / h.global_phases);
+  static const char* names[8] = {"gs", "residual", "restrict", "interp", "coarsen", "inject", "backsub", "direct"};
+  for (int k = 0; k < 16; ++k)
+    if (h.op_calls[k])
+      fprintf(stderr, "[tail]   %-7s %-8s calls %8lld  %9.0f cycles/call  %5.1f%% of tail cycles\n",
+              k < 8 ? "cluster" : "slice", names[k & 7], h.op_calls[k], (double)h.op_cyc[k] / h.op_calls[k],
+              100.0 * h.op_cyc[k] / std::max(1LL, h.cyc_total));
   for (int l = 0; l < kMaxLevels; ++l)
     if (h.lvl_gs_calls[l])
       fprintf(stderr,

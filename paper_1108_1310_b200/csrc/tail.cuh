@@ -20,6 +20,9 @@ struct TailCounters {
   long long ph_fold, ph_extra, ph_prefetch, ph_barrier;
   long long lvl_gs_cyc[kMaxLevels], lvl_gs_calls[kMaxLevels];  // per level (CTA 0, thread 0)
   long long lvl_ph[kMaxLevels][4];  // batched sweeps: first row, extra rows, prefetch, barrier
+  // K > 1: cycles and calls per operation (gs, residual, restrict, interp, coarsen, inject,
+  // backsub, direct), cluster scope [0..8) and slice scope [8..16) (leader thread)
+  long long op_cyc[16], op_calls[16];
 };
 
 // one level as the tail kernel sees it: operator (natural + colour-permuted),
@@ -45,6 +48,10 @@ struct TLevel {
   int smem_cs;  // K > 1: the operator + this CTA's column slice of x and b fit
   int gs_cta;   // K > 1 cluster tail: this level's sweeps run in CTA 0 alone (a
                 // __syncthreads per colour instead of a cluster barrier)
+  int sl_ok;    // K > 1 slice scope: x (n x 32 B) and two colour buffers of sl_cap
+  int32_t sl_cap;  // entries fit the tail CTA's dynamic shared memory (sl_rows)
+  int sl_nbuf;     // colour buffers (3: two colours in flight ahead of the fold)
+  const int32_t* sl_tab;  // [2 (ncolors + 1)] colour row ranges, then their first entries
   // workspace
   double* b;
   double* x;
@@ -82,15 +89,19 @@ struct TailPlan {
   int ctas = 64;
   int smem = kTailSmemMax;  // bytes of dynamic shared memory per tail CTA
   int32_t xs_rows = 0;      // CTA-scope sweeps keep x and b of levels this small in shared memory
+                            // (K > 1 cluster tail: subtrees rooted at levels of at most this many
+                            // rows are handed to the CTAs as 4-column slices, see SliceScope)
   bool occ2 = true;         // two tail CTAs per SM (64-register variant)
   int K = 1;                // right-hand sides per block (batch.cuh)
   int threads = 512;        // per tail CTA
   bool subtree = false;     // K > 1: plain launch, one column slice per CTA, CTA scope only
+  bool slice = false;       // K > 1 (default): K/4 independent CTAs on node-major 4-column slices
   const void* kernel = nullptr;
   DVec<TLevel> dlevels;
   DVec<double> credits;
   DVec<double> part;
   DVec<double> root_b, root_x;  // K > 1: column-major root vectors
+  DVec<int32_t> sl_tabs;        // per-level colour tables of the slice sweeps
   DVec<TailCounters> ctr;
   void build(Ctx& c, const DHier& h, Workspace& ws, int32_t max_rows);
   void reset(Ctx& c);

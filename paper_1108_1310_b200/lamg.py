@@ -806,7 +806,8 @@ class PartLevel:
 
     @classmethod
     def from_hierarchy(cls, h: Hierarchy, nparts: int, comm: Comm | None = None):
-        """The finest level of `h` split into `nparts` row blocks (lamg_part_level_from_hier)."""
+        """The first smoothing level of `h` (level 0, or level 1 below a finest
+        elimination) split into `nparts` row blocks (lamg_part_level_from_hier)."""
         self = cls.__new__(cls)
         self.ctx, self.n = h.ctx, h.n
         self.comm, self.hier = comm, h  # both must outlive the partition
@@ -815,13 +816,15 @@ class PartLevel:
         _check(self.ctx.lib.lamg_part_level_from_hier(self.ctx.p, h.h, C.c_int32(nparts), C.c_int32(first),
                                                       C.c_int32(nown), comm.p if comm is not None else None,
                                                       C.byref(self.p)))
+        self.ctx.lib.lamg_part_level_n.restype = C.c_int32
+        self.n = int(self.ctx.lib.lamg_part_level_n(self.p))  # the partitioned level's size
         return self
 
     def solve(self, h: Hierarchy, b, x0, cfg: CycleConfig | None = None):
-        """lamg_part_solve: lamg::solve with this partitioned finest level."""
+        """lamg_part_solve: lamg::solve with this partitioned level (the hierarchy's first smoothing level)."""
         cfg = cfg or CycleConfig()
         b, x0 = _f64(b), _f64(x0)
-        x = np.empty(self.n)
+        x = np.empty(h.n)
         st = _lib.lamg_solve_stats()
         cap = cfg.max_cycles + 2
         res = np.empty(cap)

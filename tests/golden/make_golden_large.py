@@ -41,6 +41,9 @@ CASES = {
     "cfg3_rgg_4M": (lambda: G.make_config(3), 103),
     "cfg4_chunglu_16M": (lambda: G.make_config(4), 104),
     "cfg5_rmat_25": (lambda: G.make_config(5), 105),
+    # config 5 at 1/8 size (the full R-MAT 25 reference run needs more host
+    # memory than the build box has): hubs of ~10^5 entries
+    "cfg5m_rmat_22": (lambda: G.rmat(22, seed=5), 105),
 }
 
 
@@ -59,7 +62,7 @@ def main(names):
         build, seed = CASES[name]
         a = build()
         b = G.gaussian_rhs(a.n, seed)
-        if name in ("cfg4_chunglu_16M", "cfg5_rmat_25"):
+        if name in ("cfg4_chunglu_16M", "cfg5_rmat_25", "cfg5m_rmat_22"):
             b = G.zero_sum(b[None])[0]  # as bench.py does for the full-size configs 4/5
         x0 = G.default_x0(a.n)
         t0 = time.time()
@@ -79,6 +82,9 @@ def main(names):
             "cycles": int(st["cycles"][0]), "residuals": [float(r) for r in st["residuals"]],
             "acf": float(st["acf"][0]), "solve_work": float(st["solve_work"][0]),
             "x_sha": sha(x), "x_norm": float(np.linalg.norm(x)),
+            # every stride-th entry of x: lets a THROUGHPUT solve be compared with the
+            # reference's solution where a VALIDATE solve is too slow to produce it
+            "x_sample_stride": max(1, a.n // 4096), "x_sample": [float(v) for v in x[::max(1, a.n // 4096)]],
             "ref_setup_s": t1 - t0, "ref_solve_s": t2 - t1,
         }
         print(f"{name}: n={a.n} m={a.m} levels={data[name]['nlevels']} cycles={data[name]['cycles']} "

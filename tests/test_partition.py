@@ -228,3 +228,60 @@ def test_partitioned_solve_bit_identical(name):
         assert np.array_equal(xp, x1), P
         pl.close()
     ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["grid5_128", "rgg_64k"])
+def test_partitioned_solve_below_a_finest_elimination(name):
+    """Hierarchies whose finest level is reduced by elimination first (2D grids,
+    geometric graphs: BASELINE configs 1 and 3): lamg_part_solve partitions
+    level 1, the first level that smooths; the finest level's RHS coarsening,
+    injection and back-substitution run replicated. Bit-identical to
+    lamg_solve (exact_levels = 0) for 1-3 parts."""
+    from paper_1108_1310_b200 import lamg as L
+    a = G.grid_5pt(128) if name == "grid5_128" else G.largest_component(G.rgg(1 << 16, seed=3))[0]
+    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    ctx.set_exact_levels(0)
+    h = L.setup(a, ctx=ctx)
+    assert h.levels[1].kind == 1 and h.levels[2].kind == 2
+    b, x0 = G.gaussian_rhs(a.n, 23), G.default_x0(a.n)
+    x1, s1 = L.solve(h, b, x0, ctx=ctx)
+    assert s1.converged and s1.residuals[-1] <= s1.residuals[0] / 1e10
+    for P in (1, 2, 3):
+        pl = L.PartLevel.from_hierarchy(h, P)
+        assert pl.n == h.levels[1].n
+        xp, sp_ = pl.solve(h, b, x0)
+        assert sp_.cycles == s1.cycles, P
+        assert np.array_equal(np.array(sp_.residuals), np.array(s1.residuals)), P
+        assert np.array_equal(xp, x1), P
+        pl.close()
+    ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["chunglu_64k", "rmat_14"])
+def test_partitioned_relaxation_coarsest(name):
+    """Configs 4 and 5 in small: finest -> elimination -> a relaxation-coarsest
+    level (coarse_solver.cpp:82-93). lamg_part_solve relaxes that level on the
+    parts (halo exchange after every colour, mean and norm over the allgathered
+    vectors): same cycle and sweep counts as lamg_solve, x within 1e-9, and
+    bit-identical for 1, 2 and 4 parts."""
+    from paper_1108_1310_b200 import lamg as L
+    a = G.largest_component(G.chung_lu(1 << 16, seed=4) if name == "chunglu_64k" else G.rmat(14, seed=5))[0]
+    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    h = L.setup(a, ctx=ctx)
+    assert h.nlevels == 2 and h.levels[1].kind == 1 and h.levels[1].coarsest == 2
+    b, x0 = G.gaussian_rhs(a.n, 29), G.default_x0(a.n)
+    x1, s1 = L.solve(h, b, x0, ctx=ctx)
+    assert s1.converged
+    xs = []
+    for P in (1, 2, 4):
+        pl = L.PartLevel.from_hierarchy(h, P)
+        xp, sp_ = pl.solve(h, b, x0)
+        assert sp_.converged and sp_.cycles == s1.cycles, P
+        assert abs(sp_.relax_sweeps - s1.relax_sweeps) <= 1, (P, sp_.relax_sweeps, s1.relax_sweeps)
+        assert np.linalg.norm(xp - x1) / np.linalg.norm(x1) <= 1e-9, P
+        xs.append(xp)
+        pl.close()
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
+    ctx.close()

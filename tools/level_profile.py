@@ -3,6 +3,9 @@ classes 2 + 4 l + {gs, residual, transfers, tail}); CUDA events around
 each kernel group, graphs off.
 
     python tools/level_profile.py [cfg] [K]     (K = 1: one-column solve)
+LANES=n runs n profiled block solves concurrently (one context each, the
+bench's arrangement) and prints lane 0's table: how much each group stretches
+under contention.
 """
 import ctypes as C
 import os
@@ -28,14 +31,23 @@ def main():
     B = np.stack([G.gaussian_rhs(a.n, 100 + cfg + 7 * i) for i in range(K)])
     X0 = np.stack([G.default_x0(a.n, seed=1 + 97 * i) for i in range(K)])
     lib = ctx.lib
-    lib.lamg_ctx_profile(ctx.p, 1)
+    lanes = int(os.environ.get("LANES", "1"))
+    mc = int(os.environ.get("MAX_CYCLES", "300"))
+    others = [L.Context(0, L.MODE_THROUGHPUT) for _ in range(lanes - 1)]
+    for c in [ctx] + others:
+        lib.lamg_ctx_profile(c.p, 1)
+    import threading
+    ths = [threading.Thread(target=lambda c=c: L.solve_batch(h, B, X0, L.CycleConfig(max_cycles=mc), ctx=c))
+           for c in others]
     t = time.time()
+    [th.start() for th in ths]
     if K == 1:
-        x, st = L.solve(h, B[0], X0[0], ctx=ctx)
+        x, st = L.solve(h, B[0], X0[0], L.CycleConfig(max_cycles=mc), ctx=ctx)
         cyc = st.cycles
     else:
-        X, st = L.solve_batch(h, B, X0, ctx=ctx)
+        X, st = L.solve_batch(h, B, X0, L.CycleConfig(max_cycles=mc), ctx=ctx)
         cyc = max(s.cycles for s in st)
+    [th.join() for th in ths]
     wall = time.time() - t
     rows = []
     tot = 0.0
