@@ -359,6 +359,20 @@ def run_lamg(args, dist: Dist):
                 k = "gs_finest_exact_order"
             kern[k + tag] = v
         log(f"[rank {dist.rank}] profiled {'block' if tag else 'single'} solve in {time.time() - tb:.1f}s")
+    if KB > 1 and "gs_finest_block" in kern:
+        # the same block with every level swept coloured (lamg_ctx_set_exact_levels(ctx, 0): the
+        # HBM-bound form of the finest sweep, which the partitioned solve uses; more cycles)
+        kern["gs_finest_block"]["note"] = ("exact-order K-column sweep (ticketed wavefront items, bgs_exact): "
+                                           "latency-bound by the front-to-front dependency chain")
+        lanes[0].ctx.set_exact_levels(0)
+        kp = kernel_profile(lib, lanes[0], Lane.solve_dev, 0.0)
+        torch.cuda.synchronize()
+        lanes[0].ctx.set_exact_levels(1)
+        if lanes[0].err:
+            raise lanes[0].err
+        if "gs_finest" in kp:
+            kp["gs_finest"]["note"] = "coloured sweep (exact_levels = 0); block converges in %d cycles" % max(lanes[0].cycles)
+            kern["gs_finest_block_coloured"] = kp["gs_finest"]
 
     for _ in range(args.warmup):
         run_lanes(lanes, Lane.solve_dev, torch, stream0)
@@ -411,8 +425,9 @@ def run_lamg(args, dist: Dist):
                                      "24n per right-hand side (x read, b read, x write); k=1 gives 24m + 40n + 8",
                 "measured": "CUDA events on the context stream around every finest-level launch of one profiled "
                             "solve inside bench.py (block: one lane's 32-column solve; single: one 1-column solve)",
-                "dominant_by_time": "subtree_kernel (the per-column coarse sub-cycle below 4096 rows) and the "
-                                    "coloured sweeps of levels 1-13: latency-bound colour phases, not HBM-bound",
+                "dominant_by_time": "tail_kernel<1,K> (the on-device sub-cycle below 16k rows: a 16-CTA cluster for "
+                                    "levels of 3k-16k rows, 4-column shared-memory slices per CTA below) and the "
+                                    "coloured sweeps of levels 1-9: latency-bound colour phases, not HBM-bound",
                 "kernels": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                             for k, v in kern.items()}}
 
