@@ -350,6 +350,43 @@ __global__ void brestrict_kernel(int32_t cn, const int64_t* __restrict__ mem_ptr
   Xc[g * K + k] = 0.0;
 }
 
+// r = b - A x and restrict_residual fused (cycle.cpp:180-186, aggregation.cpp:333-337):
+// a thread owns four columns of one aggregate, forms each member row's
+// residual exactly as bres_kernel does and folds them in member order
+// exactly as brestrict_kernel does -- the same bits, without writing and
+// re-reading R (16 n K bytes per visit). Levels without long rows only.
+template <int K, int MINB = 4>
+__global__ void __launch_bounds__(kBT, MINB) bres_restrict_kernel(CSRv a, int32_t cn,
+                                                                 const int64_t* __restrict__ mem_ptr,
+                                                                 const int32_t* __restrict__ mem,
+                                                                 const double* __restrict__ B,
+                                                                 const double* __restrict__ X, double mu,
+                                                                 double* __restrict__ Bc, double* __restrict__ Xc) {
+  constexpr int T = K / kV;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t g = t / T;
+  const int k0 = (int)(t % T) * kV;
+  if (g >= cn) return;
+  double acc[kV] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t j1 = __ldg(mem_ptr + g + 1);
+  for (int64_t j = __ldg(mem_ptr + g); j < j1; ++j) {
+    const int64_t u = __ldg(mem + j);
+    const int64_t b = __ldg(a.rp + u), e = __ldg(a.rp + u + 1);
+    const double d = __ldg(a.diag + u);
+    const d4 xu = ld4(X + u * K + k0);
+    double s[kV] = {d * xu.x, d * xu.y, d * xu.z, d * xu.w};
+    fold4<K, false>(s, a.col, a.val, X, b, e, k0);
+    const d4 bv = ld4(B + u * K + k0);
+    acc[0] = acc[0] + (bv.x - s[0]);
+    acc[1] = acc[1] + (bv.y - s[1]);
+    acc[2] = acc[2] + (bv.z - s[2]);
+    acc[3] = acc[3] + (bv.w - s[3]);
+  }
+  if (mu != 1.0) st4(Bc + g * K + k0, acc[0] * mu, acc[1] * mu, acc[2] * mu, acc[3] * mu);
+  else st4(Bc + g * K + k0, acc[0], acc[1], acc[2], acc[3]);
+  st4(Xc + g * K + k0, 0.0, 0.0, 0.0, 0.0);
+}
+
 template <int K>
 __global__ void binterp_kernel(int32_t n, const int32_t* __restrict__ agg, const double* __restrict__ Xc,
                                double* __restrict__ X) {
@@ -613,6 +650,23 @@ void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const 
     }
   });
   CK_LAUNCH();
+}
+
+bool bresidual_restrict(Ctx& c, const CSRv& a, const LongRows& L, int32_t coarse_n, const int64_t* mem_ptr,
+                        const int32_t* mem, const double* B, const double* X, double mu, double* Bc, double* Xc,
+                        int K) {
+  static const bool off = [] {
+    const char* e = getenv("LAMG_NO_FUSED_RESTRICT");
+    return e && atoi(e) == 1;
+  }();
+  if (off || a.n == 0 || coarse_n == 0 || L.ptr_h.empty() || L.ptr_h[1] || L.iptr_h[1]) return false;
+  dispatch_k(K, [&](auto kc) {
+    constexpr int KK = decltype(kc)::value;
+    count_launch(), bres_restrict_kernel<KK><<<bblocks((int64_t)coarse_n * (KK / kV)), kBT, 0, c.s>>>(
+        a, coarse_n, mem_ptr, mem, B, X, mu, Bc, Xc);
+  });
+  CK_LAUNCH();
+  return true;
 }
 
 void brestrict(Ctx& c, int32_t coarse_n, const int64_t* mem_ptr, const int32_t* mem, const double* R, double mu,

@@ -79,6 +79,11 @@ void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X
 void bgs_exact(Ctx& c, const CSRv& a, const Schedule& sch, const ExactItems& it, const double* B, double* X,
                int sweeps, int K, int32_t* ctl);
 void bresidual(Ctx& c, const CSRv& a, const LongRows& L, const double* B, const double* X, double* R, int K);
+// residual + restriction in one pass (bit-identical to bresidual then brestrict);
+// false when the level has long rows (the caller runs the two kernels)
+bool bresidual_restrict(Ctx& c, const CSRv& a, const LongRows& L, int32_t coarse_n, const int64_t* mem_ptr,
+                        const int32_t* mem, const double* B, const double* X, double mu, double* Bc, double* Xc,
+                        int K);
 void brestrict(Ctx& c, int32_t coarse_n, const int64_t* mem_ptr, const int32_t* mem, const double* R, double mu,
                double* Bc, double* Xc, int K);
 void binterpolate(Ctx& c, int32_t fine_n, const int32_t* agg, const double* Xc, double* X, int K);

@@ -415,7 +415,14 @@ struct Driver {
     int nsaved = 0;
     for (int i = 0; i < theta; ++i) {
       if (child.nu_pre) gs(l, b, x, child.nu_pre);
-      resid(l, b, x, w.r.p);
+      // K-column blocks: residual and restriction in one kernel where the level has no long rows
+      bool fused = false;
+      if (K > 1 && !adaptive && !c.prof.enabled) {
+        fused = bresidual_restrict(c, L.op.view(), L.blong_nat, t.coarse_n, t.mem_ptr.p, t.mem.p, b, x, cfg.mu,
+                                   wc.b.p, wc.x.p, K);
+        if (fused) c.work += (double)L.op.m;
+      }
+      if (!fused) resid(l, b, x, w.r.p);
       if (trace && K == 1)
         fprintf(stderr, "[trace]   l=%zu pre-smoothed |x|=%.6e |r|=%.6e\n", l, tnorm(x, L.op.n), tnorm(w.r.p, L.op.n));
       if (adaptive) {
@@ -425,7 +432,8 @@ struct Driver {
         ++nsaved;
       }
       prof_mark(c, pcls(l, 2), true);
-      if (K > 1) {
+      if (fused) {
+      } else if (K > 1) {
         brestrict(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p, wc.x.p, K);
       } else {
         restrict_exact(c, t.coarse_n, t.mem_ptr.p, t.mem.p, w.r.p, cfg.mu, wc.b.p);

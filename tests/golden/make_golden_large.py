@@ -62,8 +62,8 @@ def main(names):
         build, seed = CASES[name]
         a = build()
         b = G.gaussian_rhs(a.n, seed)
-        if name in ("cfg4_chunglu_16M", "cfg5_rmat_25", "cfg5m_rmat_22"):
-            b = G.zero_sum(b[None])[0]  # as bench.py does for the full-size configs 4/5
+        if name in ("cfg3_rgg_4M", "cfg4_chunglu_16M", "cfg5_rmat_25", "cfg5m_rmat_22"):
+            b = G.zero_sum(b[None])[0]  # as bench.py does for the full-size configs 3-5
         x0 = G.default_x0(a.n)
         t0 = time.time()
         h = ref.setup(a)

@@ -77,7 +77,7 @@ def test_large_config_matches_reference_digests(name):
 # are generated on the device and their digests checked against the host
 # restatement the reference consumed.
 FULL = {
-    "cfg3_rgg_4M": dict(host=lambda: G.make_config(3), validate=True),
+    "cfg3_rgg_4M": dict(host=lambda: G.make_config(3), zero_sum=True, validate=True),
     "cfg4_chunglu_16M": dict(dev=lambda L, ctx: L.gen_chung_lu(1 << 24, seed=4, ctx=ctx), zero_sum=True,
                              validate=False),
     "cfg5m_rmat_22": dict(dev=lambda L, ctx: L.gen_rmat(22, seed=5, ctx=ctx), zero_sum=True, validate=False),
