@@ -410,7 +410,7 @@ def run_lamg(args, dist: Dist):
     dom = "gs_finest_block" if "gs_finest_block" in kern else ("gs_finest_exact_order" if "gs_finest_exact_order" in kern else None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if dom and os.path.exists(tp):
+    if dom and args.config == 2 and os.path.exists(tp):  # the captures are of config 2's finest level
         t = json.load(open(tp)).get(f"{args.mode}:{dom}")
         if isinstance(t, dict):  # per sweep -> per profiled launch (one gs call = nu sweeps)
             kk = t["k"]

@@ -373,7 +373,8 @@ struct Driver {
   static int pcls(size_t l, int k) { return 2 + 4 * (int)std::min<size_t>(l, 63) + k; }
   void gs(size_t l, const double* b, double* x, int sweeps) {
     const DLevel& L = *h.levels[l];
-    const bool p = l == 0;
+    // profile class 0: the sweeps of the finest level that smooths (level 1 below a finest elimination)
+    const bool p = (int)l == exact_levels() - c.exact_levels;
     if (p) prof_mark(c, 0, true);
     prof_mark(c, pcls(l, 0), true);
     if (K > 1) {

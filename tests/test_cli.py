@@ -61,8 +61,8 @@ def test_cli_error_objects_and_exit_codes(tmp_path):
 
 
 def _disconnected():
-    """A 12x12 grid, a 7-node path and an isolated node."""
-    g, p = G.grid_5pt(12), G.path(7)
+    """A 16x16 grid, a 7-node path and an isolated node."""
+    g, p = G.grid_5pt(16), G.path(7)
     n = g.n + p.n + 1
     u, v, w = [], [], []
     for a, off in ((g, 0), (p, g.n)):
@@ -84,8 +84,8 @@ def test_cli_solve_info_bench_match_the_oracle(tmp_path):
     mtx = str(tmp_path / "a.mtx")
     L.write_matrix_market(mtx, a)
     b = np.zeros(a.n)
-    b[:144] = G.gaussian_rhs(144, 7)
-    b[144:151] = [1.0, 0.0, -1.0, 0.5, -0.25, -0.25, 0.0]
+    b[:256] = G.gaussian_rhs(256, 7)
+    b[256:263] = [1.0, 0.0, -1.0, 0.5, -0.25, -0.25, 0.0]
     bfile = tmp_path / "b.txt"
     bfile.write_text("\n".join(repr(float(v)) for v in b) + "\n")
     xfile, sfile = str(tmp_path / "x.txt"), str(tmp_path / "s.json")
@@ -117,7 +117,7 @@ def test_cli_solve_info_bench_match_the_oracle(tmp_path):
     # info: the largest component's hierarchy, level by level
     rc, out, _ = run("info", "--matrix", mtx)
     info = json.loads(out)
-    g12 = G.grid_5pt(12)
+    g12 = G.grid_5pt(16)
     assert rc == 0 and info["components"] == 3 and len(info["levels"]) >= 2
     assert (info["levels"][0]["n"], info["levels"][0]["m"], info["levels"][0]["kind"]) == (g12.n, g12.m, "finest")
     assert info["levels"][-1]["coarsest"] is True and info["setup_mvm"] == pytest.approx(st["setup_mvm"], rel=1e-12)

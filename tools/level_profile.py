@@ -25,9 +25,11 @@ def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     K = int(sys.argv[2]) if len(sys.argv) > 2 else 32
     a = config(cfg)
-    ctx = L.Context(0, L.MODE_THROUGHPUT)
+    validate = os.environ.get("MODE", "throughput") == "validate"  # MODE=validate: the exact-order solve (K = 1)
+    ctx = L.Context(0, L.MODE_VALIDATE if validate else L.MODE_THROUGHPUT)
     h = L.setup(a, ctx=ctx)
-    h.prepare_throughput()
+    if not validate:
+        h.prepare_throughput()
     B = np.stack([G.gaussian_rhs(a.n, 100 + cfg + 7 * i) for i in range(K)])
     X0 = np.stack([G.default_x0(a.n, seed=1 + 97 * i) for i in range(K)])
     lib = ctx.lib
