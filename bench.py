@@ -578,7 +578,16 @@ def run_reference(args, dist: Dist):
         tot += secs
         units += float(c.sum()) * a.m
     v = units / tot
+    # time to solution from the per-cycle rate and the reference's own cycle count to 1e-10
+    # (tests/golden/large.json: the compiled reference's full solve of this operator)
+    gl = os.path.join(ROOT, "tests", "golden", "large.json")
+    key = {1: "cfg1_grid5_256", 2: "cfg2_grid3d_128", 3: "cfg3_rgg_4M", 4: "cfg4_chunglu_16M"}.get(args.config)
+    ref_cycles = json.load(open(gl)).get(key, {}).get("cycles") if key and os.path.exists(gl) else None
+    rhs_per_s = v / (a.m * ref_cycles) if ref_cycles else None
     return {"metric": "fine-level edges*cycles/s (solve to relative residual 1e-10)", "value": v,
+            "rhs_solved_per_s": rhs_per_s,
+            "rhs_solved_per_s_basis": (f"value / (m x {ref_cycles} cycles: the reference's full solve of this operator, "
+                                       "tests/golden/large.json)") if ref_cycles else None,
             "unit": "edges*cycles/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic: seeded generator for BASELINE.json config %d" % args.config,

@@ -136,6 +136,9 @@ const char *lamg_last_error(void);
 const char *lamg_version(void);
 /* kernels this library has launched so far (all contexts, monotone) */
 int64_t lamg_launch_count(void);
+/* LAMG_GUARD=1 (debugging aid): device buffers carry 256-byte guard bands checked at
+ * release; buffers checked so far and overruns found (also reported on stderr) */
+void lamg_guard_report(int64_t *checked, int64_t *overruns);
 /* the context's cudaStream_t, for callers that time or order work with it */
 void *lamg_ctx_stream(lamg_ctx *ctx);
 

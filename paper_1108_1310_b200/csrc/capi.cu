@@ -247,6 +247,12 @@ const char* lamg_last_error(void) { return g_err.c_str(); }
 const char* lamg_version(void) { return "lamg_b200 0.1 (sm_100a)"; }
 
 int64_t lamg_launch_count(void) { return (int64_t)g_launches.load(); }
+void lamg_guard_report(int64_t* checked, int64_t* overruns) {
+  long long c = 0, o = 0;
+  guard_report(&c, &o);
+  if (checked) *checked = c;
+  if (overruns) *overruns = o;
+}
 
 void* lamg_ctx_stream(lamg_ctx* ctx) { return ctx ? (void*)ctx->c.s : nullptr; }
 

@@ -1,7 +1,9 @@
 // common.cu -- context, error mapping, CUB wrappers and the bit-exact folds.
 #include <cub/cub.cuh>
 
+#include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <string>
 
 #include "common.cuh"
@@ -353,6 +355,51 @@ void tree_norm2(Ctx& c, const double* x, int64_t n, double* d_out) {
   count_launch(), tree_partial_kernel<true><<<nb, kThreads, 0, c.s>>>(x, n, part);
   count_launch(), tree_final_kernel<true><<<1, 256, 0, c.s>>>(part, nb, d_out);
   CK_LAUNCH();
+}
+
+// ------------------------------------------------------- guard bands (LAMG_GUARD=1)
+namespace {
+__global__ void guard_fill_kernel(unsigned char* base, size_t payload) {
+  const size_t t = threadIdx.x;  // kGuardBytes threads
+  base[t] = (unsigned char)(0xA5 ^ t);
+  base[kGuardBytes + payload + t] = (unsigned char)(0x5A ^ t);
+}
+__global__ void guard_check_kernel(const unsigned char* base, size_t payload, unsigned long long* bad) {
+  const size_t t = threadIdx.x;
+  if (base[t] != (unsigned char)(0xA5 ^ t)) atomicMin(bad, (unsigned long long)t);
+  if (base[kGuardBytes + payload + t] != (unsigned char)(0x5A ^ t)) atomicMin(bad + 1, (unsigned long long)t);
+}
+std::atomic<long long> g_guard_checked{0}, g_guard_overruns{0};
+}  // namespace
+
+void guard_fill(void* base, size_t payload, cudaStream_t s) {
+  guard_fill_kernel<<<1, (unsigned)kGuardBytes, 0, s>>>((unsigned char*)base, payload);
+}
+
+void guard_check(const void* base, size_t payload, cudaStream_t s, bool sync_free) {
+  // a small synchronous check: debugging mode only
+  unsigned long long* bad = nullptr;
+  if (cudaMalloc((void**)&bad, 2 * sizeof(unsigned long long)) != cudaSuccess) return;
+  cudaMemset(bad, 0xff, 2 * sizeof(unsigned long long));
+  cudaStream_t st = sync_free ? 0 : s;
+  if (sync_free) cudaDeviceSynchronize();
+  guard_check_kernel<<<1, (unsigned)kGuardBytes, 0, st>>>((const unsigned char*)base, payload, bad);
+  unsigned long long h[2] = {~0ull, ~0ull};
+  cudaMemcpyAsync(h, bad, sizeof h, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(bad);
+  ++g_guard_checked;
+  for (int k = 0; k < 2; ++k)
+    if (h[k] != ~0ull) {
+      ++g_guard_overruns;
+      fprintf(stderr, "[lamg guard] buffer of %zu bytes: %s band overwritten (first bad byte at offset %llu)\n", payload,
+              k ? "trailing" : "leading", h[k]);
+    }
+}
+
+void guard_report(long long* checked, long long* overruns) {
+  *checked = g_guard_checked.load();
+  *overruns = g_guard_overruns.load();
 }
 
 }  // namespace lamgb

@@ -98,6 +98,21 @@ inline bool poison_enabled() {
   return on;
 }
 
+// LAMG_GUARD=1 (debugging aid; compute-sanitizer is not available on the GPU
+// pool): every device buffer is allocated with a 256-byte band of a known
+// pattern before and after it, and the bands are checked when the buffer is
+// released -- an out-of-bounds write next to any buffer is reported on stderr
+// (buffer size, which band, first bad offset) and counted
+// (lamg_guard_report: buffers checked / overruns).
+inline bool guard_enabled() {
+  static const bool on = getenv("LAMG_GUARD") && atoi(getenv("LAMG_GUARD")) == 1;
+  return on;
+}
+constexpr size_t kGuardBytes = 256;
+void guard_fill(void* base, size_t payload, cudaStream_t s);          // common.cu
+void guard_check(const void* base, size_t payload, cudaStream_t s, bool sync_free);  // common.cu
+void guard_report(long long* checked, long long* overruns);
+
 template <typename T>
 struct DVec {
   T* p = nullptr;
@@ -121,14 +136,26 @@ struct DVec {
     release();
     s = st;
     n = count;
-    if (count > 0) CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, s));
+    if (count > 0 && guard_enabled()) {
+      unsigned char* base = nullptr;
+      CK(cudaMallocAsync((void**)&base, sizeof(T) * (size_t)count + 2 * kGuardBytes, s));
+      guard_fill(base, sizeof(T) * (size_t)count, s);
+      p = (T*)(base + kGuardBytes);
+    } else if (count > 0) {
+      CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, s));
+    }
     // LAMG_POISON=1 (debugging aid): fresh floating-point buffers start as NaN,
     // so a read of never-written memory shows up in the results
     if constexpr (std::is_floating_point<T>::value)
       if (count > 0 && poison_enabled()) CK(cudaMemsetAsync(p, 0xff, sizeof(T) * (size_t)count, s));
   }
   void release() {
-    if (p) {
+    if (p && guard_enabled()) {
+      unsigned char* base = (unsigned char*)p - kGuardBytes;
+      guard_check(base, sizeof(T) * (size_t)n, s, g_free_sync);
+      if (g_free_sync) cudaFree(base);
+      else cudaFreeAsync(base, s);
+    } else if (p) {
       if (g_free_sync) cudaFree(p);
       else cudaFreeAsync(p, s);
     }

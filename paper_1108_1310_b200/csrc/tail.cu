@@ -1986,6 +1986,10 @@ void TailPlan::reset(Ctx& c) {
 }
 
 void TailPlan::run(Ctx& c, int l, int theta, double mu, int nlevels) {
+  // LAMG_SKIP_TAIL=1 (timing experiments only: wrong results): the sub-cycle below
+  // the host-driven levels is not run, which isolates the cost of the levels above
+  static const bool skip = getenv("LAMG_SKIP_TAIL") && atoi(getenv("LAMG_SKIP_TAIL")) == 1;
+  if (skip) return;
   const TLevel* lv = dlevels.p;
   double* cr = credits.p;
   double* pt = part.p;

@@ -745,63 +745,6 @@ void residual_tasks(Ctx& c, const CSRv& a, const LongRows& nat, const double* b,
   CK_LAUNCH();
 }
 
-// L2 persistence for the relaxation iterate. x (8n bytes: 67 MB on config 5) is
-// gathered 2m/n ~ 120 times per sweep while 24m bytes of operator stream
-// through L2 once and evict it: ncu counts 30.6 GB of DRAM traffic per sweep
-// for 12.8 GB of algorithmic bytes on R-MAT 25 (every missed 8-byte gather
-// moves a 32-byte sector). The access policy window marks accesses to x as
-// persisting and everything else the kernels touch as streaming. Kernel nodes
-// of a captured graph do not inherit the stream attribute, so the window is
-// set on every kernel node before instantiation.
-struct L2Window {
-  cudaAccessPolicyWindow w = {};
-  bool on = false;
-  L2Window(const void* p, size_t bytes) {
-    static const bool off = [] {
-      const char* e = getenv("LAMG_L2_PIN");
-      return e && atoi(e) == 0;
-    }();
-    if (off || !p || !bytes) return;
-    int dev = 0, max_persist = 0, max_window = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    if (max_persist <= 0 || max_window <= 0) return;
-    const size_t want = std::min<size_t>(bytes, (size_t)max_persist);
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
-      cudaGetLastError();
-      return;
-    }
-    w.base_ptr = const_cast<void*>(p);
-    w.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
-    w.hitRatio = (float)std::min(1.0, (double)want / (double)w.num_bytes);
-    w.hitProp = cudaAccessPropertyPersisting;
-    w.missProp = cudaAccessPropertyStreaming;
-    on = true;
-    if (getenv("LAMG_RELAX_TRACE"))
-      fprintf(stderr, "[relax] L2 window %zu bytes (persisting limit %zu of max %d, max window %d), hit ratio %.2f\n",
-              w.num_bytes, want, max_persist, max_window, w.hitRatio);
-  }
-  void apply(cudaGraph_t graph) const {
-    if (!on) return;
-    size_t nn = 0;
-    if (cudaGraphGetNodes(graph, nullptr, &nn) != cudaSuccess || !nn) return;
-    std::vector<cudaGraphNode_t> nodes(nn);
-    if (cudaGraphGetNodes(graph, nodes.data(), &nn) != cudaSuccess) return;
-    for (cudaGraphNode_t nd : nodes) {
-      cudaGraphNodeType t;
-      if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
-      cudaKernelNodeAttrValue v = {};
-      v.accessPolicyWindow = w;
-      if (cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v) != cudaSuccess)
-        cudaGetLastError();
-    }
-  }
-  ~L2Window() {
-    if (on) cudaCtxResetPersistingL2Cache();
-  }
-};
-
 // RelaxationSolver::solve (coarse_solver.cpp:82-93), THROUGHPUT, for large
 // relaxation-coarsest levels: per sweep one CUDA graph (a task launch per
 // colour, mean subtraction, residual, norm), the convergence test on the
@@ -858,7 +801,6 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
   // the sweep graph is cached per context (its scratch pointers are the
   // context's), keyed by the colouring's uid, the natural operator, the
   // vectors and the scratch generation
-  const L2Window l2(x, (size_t)a.n * sizeof(double));
   Ctx::RelaxGraph& g = c.relax_graph;
   if (!g.exec || g.key != cl.uid || g.op != a.val || g.b != b || g.x != x || g.r != r || g.gen != c.rgen) {
     if (g.exec) CK(cudaGraphExecDestroy(g.exec));
@@ -868,7 +810,6 @@ int relax_colored_graph(Ctx& c, const CSRv& a, const DColor& cl, const LongRows&
     CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
     sweep();
     CK(cudaStreamEndCapture(c.s, &graph));
-    l2.apply(graph);
     CK(cudaGraphInstantiate(&g.exec, graph, 0));
     CK(cudaGraphDestroy(graph));
     g.launches = t_launches - l0;

@@ -101,7 +101,8 @@ def test_cli_solve_info_bench_match_the_oracle(tmp_path):
     assert np.array_equal(x, xo)  # VALIDATE: the reference's iterate, bit for bit
     assert (st["n"], st["m"], st["components"]) == (a.n, a.m, 3)
     assert st["converged"] is True and st["cycles"] == int(rep["cycles"][0])
-    assert st["solve_mvm"] == pytest.approx(float(rep["solve_work"][0]), rel=1e-12)
+    assert st["solve_mvm"] == pytest.approx(float(rep["total_solve_work"][0]), rel=1e-12)
+    assert st["setup_mvm"] == pytest.approx(float(op.export()["setup_work"][0]), rel=1e-12)
     assert st["correction"] == "flat" and st["seed"] == 1
     for k in ("acf", "residual_initial", "residual_final", "reduction", "setup_mvm", "total_mvm", "t_setup",
               "t_solve", "t_total", "setup_fraction", "storage_per_edge", "edge_ratio", "recombinations",

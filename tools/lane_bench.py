@@ -34,6 +34,8 @@ def main():
     lanes = [bench.Lane(L, torch, 0, h, L.MODE_THROUGHPUT, B, X0) for _ in range(NL)]
     for ln in lanes:
         ln.cfg.max_cycles = mc
+        if "LAMG_EXACT_LEVELS" in os.environ:  # 0: every level coloured
+            ln.ctx.set_exact_levels(int(os.environ["LAMG_EXACT_LEVELS"]))
     s0 = lanes[0].stream
     out = []
     for n in sorted({1, NL}):

@@ -1,5 +1,13 @@
-"""Workload for compute-sanitizer (memcheck / racecheck / synccheck, one tool
-per run): the smoke solve, one power-law THROUGHPUT solve (relaxation
+"""Memory-safety workload. compute-sanitizer is closed on the GPU pool, so the
+library's own guard mode stands in: LAMG_GUARD=1 puts 256-byte pattern bands
+around every device buffer and checks them at release (LAMG_POISON=1 also
+fills fresh floating-point buffers with NaN, so reads of never-written memory
+surface in the compared results). Where compute-sanitizer is available the
+same script is the workload for --tool memcheck / racecheck / synccheck.
+
+    LAMG_GUARD=1 LAMG_POISON=1 python tools/sanitize_workload.py
+
+The workload: the smoke solve, one power-law THROUGHPUT solve (relaxation
 coarsest with chunked hub rows and acq_rel chunk counters, two contexts
 sharing the hierarchy), and one 32-column THROUGHPUT block (bgs_exact tickets,
 the node-major cluster tail).
@@ -44,4 +52,14 @@ assert all(s.converged for s in st)
 print(f"32-column block: n={g.n} cycles={st[0].cycles}..{max(s.cycles for s in st)}")
 c2.close()
 ctx.close()
+del h, hg
+import ctypes as C  # noqa: E402
+import gc  # noqa: E402
+
+gc.collect()
+chk, ovr = C.c_int64(), C.c_int64()
+L._lib.lib().lamg_guard_report(C.byref(chk), C.byref(ovr))
+print(f"guard bands: {chk.value} buffers checked, {ovr.value} overruns"
+      + ("" if os.environ.get("LAMG_GUARD") == "1" else " (LAMG_GUARD not set: nothing checked)"))
+assert ovr.value == 0
 print("sanitize workload ok")
