@@ -4,7 +4,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lamg|reference]
                     [--mode throughput|validate] [--config 1..5] [--lanes 8] [--block 32]
 
-A step solves lanes x block right-hand sides (default 8 x 32), each to the
+A step solves lanes x block right-hand sides (default 8 x 64), each to the
 reference's relative residual 1e-10, on BASELINE.json config 2 -- the 3D
 7-point 128^3 Laplacian with seeded log-uniform weights -- over a hierarchy
 built once on the GPU (setup is timed separately and reported; configs 4 and
@@ -115,6 +115,11 @@ WORKLOADS = {
        "the device), Gaussian zero-sum b, to 1e-10",
 }
 DEFAULT_LANES = {1: 8, 2: 8, 3: 8, 4: 2, 5: 2}
+# right-hand sides per lane: 64 on the grid-like configs (tools/lane_bench.py on config 2:
+# 8 x 32 9.1e9, 8 x 64 1.14e10, 4 x 128 1.01e10 edges*cycles/s -- the ~800 latency-bound colour
+# launches of a lane-cycle are shared by twice the columns); 32 on the power-law configs,
+# whose blocks are bound by their X gathers
+DEFAULT_BLOCK = {1: 64, 2: 64, 3: 32, 4: 32, 5: 32}  # config 3: 8 x 64 blocks of 4.2M rows exceed one GPU
 
 
 def rhs_seed(cfg: int, rank: int, i: int) -> int:
@@ -295,7 +300,7 @@ def run_lamg(args, dist: Dist):
 
     dev = dist.local
     torch.cuda.set_device(dev)
-    NL, KB = args.lanes or DEFAULT_LANES[args.config], args.block
+    NL, KB = args.lanes or DEFAULT_LANES[args.config], args.block or DEFAULT_BLOCK[args.config]
     mode = L.MODE_THROUGHPUT if args.mode == "throughput" else L.MODE_VALIDATE
     ctx0 = L.Context(dev, mode)
     lib = ctx0.lib
@@ -424,7 +429,9 @@ def run_lamg(args, dist: Dist):
                 "algorithmic_bytes": "per finest Gauss-Seidel sweep: operator once (8(n+1) + 24m + 8n) plus "
                                      "24n per right-hand side (x read, b read, x write); k=1 gives 24m + 40n + 8",
                 "measured": "CUDA events on the context stream around every finest-level launch of one profiled "
-                            "solve inside bench.py (block: one lane's 32-column solve; single: one 1-column solve)",
+                            "solve inside bench.py (block: one lane's K-column solve; single: one 1-column solve); "
+                            "traffic: ncu DRAM bytes of a 32-column sweep (profiles/traffic.json) scaled by the "
+                            "algorithmic bytes of this block width",
                 "dominant_by_time": "tail_kernel<1,K> (the on-device sub-cycle below 16k rows: a 16-CTA cluster for "
                                     "levels of 3k-16k rows, 4-column shared-memory slices per CTA below) and the "
                                     "coloured sweeps of levels 1-9: latency-bound colour phases, not HBM-bound",
@@ -628,7 +635,8 @@ def main():
     ap.add_argument("--cpu-cycles", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=0,
                     help="concurrent solve lanes (contexts/streams) per GPU (0: 8, configs 4/5: 2)")
-    ap.add_argument("--block", type=int, default=32, help="right-hand sides per lane (1..128; 1 = single solves)")
+    ap.add_argument("--block", type=int, default=0,
+                    help="right-hand sides per lane (1..128; 1 = single solves; 0: 64, configs 3-5: 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-validate", action="store_true")
     ap.add_argument("--validate-big", action="store_true",

@@ -85,6 +85,74 @@ __global__ void __launch_bounds__(kBT, MINB) bgs_kernel(const int64_t* __restric
   }
 }
 
+// The same colour launch with programmatic dependent launch (sm_90+): on the
+// coarser host-driven levels a colour is ONE wave of CTAs whose life is three
+// dependent round trips (row extent -> entries -> x gathers) after ~2 us of
+// launch latency. Launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// the grid starts while the previous colour is still running, loads everything
+// that no earlier launch writes (row extent, row id, diagonal, the first eight
+// entries), waits for the previous grid to complete and flush
+// (griddepcontrol.wait), lets the next colour start its own prologue
+// (griddepcontrol.launch_dependents) and only then reads b, gathers x, folds
+// in entry order (the arithmetic of bgs_kernel) and stores.
+template <int K>
+__global__ void __launch_bounds__(kBT, 4) bgs_pdl_kernel(const int64_t* __restrict__ rp,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ diag,
+                                                         const int32_t* __restrict__ row_ids, int32_t i0, int32_t i1,
+                                                         const double* B, double* X, const int32_t* done) {
+  constexpr int T = K / kV;
+  constexpr int U = 8;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = i0 + t / T;
+  const int k0 = (int)(t % T) * kV;
+  const bool act = i < i1;
+  int64_t b = 0, e = 0;
+  int32_t u = 0;
+  double d = 1.0;
+  int32_t c[U];
+  double v[U];
+  if (act) {
+    b = __ldg(rp + i);
+    e = __ldg(rp + i + 1);
+    u = __ldg(row_ids + i);
+    d = __ldg(diag + i);
+  }
+  const bool mine = act && e - b <= kLongRow;  // long rows: bgs_long_kernel / blong_*_kernel
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    const bool ok = mine && b + j < e;
+    c[j] = ok ? __ldg(col + b + j) : 0;
+    v[j] = ok ? __ldg(val + b + j) : 0.0;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!mine) return;
+  const d4 bv = ld4(B + (int64_t)u * K + k0);
+  d4 xv[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) xv[j] = b + j < e ? ld4(X + (int64_t)c[j] * K + k0) : d4{0.0, 0.0, 0.0, 0.0};
+  double s[kV] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (b + j < e) {
+      s[0] = s[0] - v[j] * xv[j].x;
+      s[1] = s[1] - v[j] * xv[j].y;
+      s[2] = s[2] - v[j] * xv[j].z;
+      s[3] = s[3] - v[j] * xv[j].w;
+    }
+  if (e - b > U) fold4<K, true>(s, col, val, X, b + U, e, k0);
+  double* px = X + (int64_t)u * K + k0;
+  if (done) {
+#pragma unroll
+    for (int q = 0; q < kV; ++q)
+      if (!done[k0 + q]) px[q] = s[q] / d;
+  } else {
+    st4(px, s[0] / d, s[1] / d, s[2] / d, s[3] / d);
+  }
+}
+
 // ---------------------------------------------- exact-order block sweep
 // gauss_seidel_sweep (smoothing.cpp:29-40) in the reference's row order for
 // K columns at once, without a grid barrier: the level's wavefronts (rows
@@ -574,14 +642,39 @@ void bgs_colored(Ctx& c, const DColor& cl, int32_t n, const double* B, double* X
   if (n == 0 || sweeps <= 0) return;
   const LongRows& L = cl.blong;
   double* scratch = long_scratch(c, L, K);
+  // LAMG_PDL_THREADS=t: colour launches of at most t threads (about one wave: 148 SMs x
+  // 1024 = 160000) go through programmatic dependent launch
+  static const int64_t pdl_threads = [] {
+    const char* e = getenv("LAMG_PDL_THREADS");
+    return e ? atoll(e) : (int64_t)0;  // off by default: measured 74.6 -> 72.4 ms per block cycle for one
+                                        // lane on config 2, no gain with 8 lanes in flight (LAMG_PDL_THREADS=160000)
+  }();
   dispatch_k(K, [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
     for (int sw = 0; sw < sweeps; ++sw)
       for (int32_t cc = 0; cc < cl.ncolors; ++cc) {
         const int32_t i0 = cl.cptr_h[cc], i1 = cl.cptr_h[cc + 1];
         if (i1 <= i0) continue;
-        count_launch(), bgs_kernel<KK><<<bblocks((int64_t)(i1 - i0) * (KK / kV)), kBT, 0, c.s>>>(
-            cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, i0, i1, B, X, done);
+        const int64_t nthreads = (int64_t)(i1 - i0) * (KK / kV);
+        if (pdl_threads > 0 && nthreads <= pdl_threads) {
+          // one-wave colours: programmatic dependent launch (see bgs_pdl_kernel)
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)bblocks(nthreads));
+          cfg.blockDim = dim3(kBT);
+          cfg.stream = c.s;
+          cudaLaunchAttribute at;
+          at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at.val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = &at;
+          cfg.numAttrs = 1;
+          count_launch();
+          CK(cudaLaunchKernelEx(&cfg, bgs_pdl_kernel<KK>, (const int64_t*)cl.rp.p, (const int32_t*)cl.col.p,
+                                (const double*)cl.val.p, (const double*)cl.diag.p, (const int32_t*)cl.row_ids.p, i0,
+                                i1, B, X, done));
+        } else {
+          count_launch(), bgs_kernel<KK><<<bblocks(nthreads), kBT, 0, c.s>>>(
+              cl.rp.p, cl.col.p, cl.val.p, cl.diag.p, cl.row_ids.p, i0, i1, B, X, done);
+        }
         const int32_t nl = L.ptr_h[cc + 1] - L.ptr_h[cc];
         if (nl)
           count_launch(), bgs_long_kernel<KK><<<nl, kBT, 0, c.s>>>(cl.rp.p, cl.col.p, cl.val.p, cl.diag.p,
