@@ -367,8 +367,9 @@ def run_lamg(args, dist: Dist):
     if KB > 1 and "gs_finest_block" in kern:
         # the same block with every level swept coloured (lamg_ctx_set_exact_levels(ctx, 0): the
         # HBM-bound form of the finest sweep, which the partitioned solve uses; more cycles)
-        kern["gs_finest_block"]["note"] = ("exact-order K-column sweep (ticketed wavefront items, bgs_exact): "
-                                           "latency-bound by the front-to-front dependency chain")
+        kern["gs_finest_block"]["note"] = ("the benchmarked finest sweep: front-modulo colouring (colour = wavefront mod "
+                                           "64: the reference's row order except at the wrap, 64 launches of "
+                                           "bgs_kernel per sweep; LAMG_FRONT_MOD=0 gives the exact-order bgs_exact)")
         lanes[0].ctx.set_exact_levels(0)
         kp = kernel_profile(lib, lanes[0], Lane.solve_dev, 0.0)
         torch.cuda.synchronize()

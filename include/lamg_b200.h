@@ -125,11 +125,14 @@ typedef struct {
 /* ---- context ---------------------------------------------------------- */
 int lamg_ctx_create(int device, int mode, lamg_ctx **out);
 int lamg_ctx_set_mode(lamg_ctx *ctx, int mode);
-/* THROUGHPUT one-column solves: how many of the finest SMOOTHING levels keep
- * the reference's exact Gauss-Seidel order (default 1; 0 = every level
+/* THROUGHPUT solves: how many of the finest SMOOTHING levels keep the
+ * reference's Gauss-Seidel row order (default 1; 0 = every level greedy-
  * coloured). The first smoothing level's order decides the cycle count
- * (config 2: exact 129 = the reference's, coloured 141; RGG 2^20: 13 vs 15).
- * Blocks of columns and partitioned solves sweep coloured. */
+ * (config 2: 129 = the reference's, greedy-coloured 141; RGG 2^20: 13 vs 15).
+ * One-column solves sweep those levels in exact order (wavefronts); blocks of
+ * columns sweep them with colours = wavefront mod 64 (the reference's order
+ * except at the wrap; environment LAMG_FRONT_MOD, 0 = exact order by
+ * ticketed wavefront items). Partitioned solves sweep greedy-coloured. */
 int lamg_ctx_set_exact_levels(lamg_ctx *ctx, int32_t levels);
 void lamg_ctx_destroy(lamg_ctx *ctx);
 const char *lamg_last_error(void);

@@ -139,6 +139,7 @@ struct DLevel {
   std::unique_ptr<DDirect> direct;
   Schedule sched;          // exact-order GS wavefronts of this level's operator
   std::unique_ptr<DColor> color;  // throughput-mode coloured operator (on demand)
+  std::unique_ptr<DColor> fcolor;  // front-modulo colouring of the finest smoothing level (LAMG_FRONT_MOD)
   ExactItems xitems[kExactTables];  // throughput mode: exact-order K-column sweep items (per item size)
   LongRows blong_nat;             // throughput mode: long rows in natural order (K-column residuals)
   UpperIndex upper;        // energy / relaxation helpers

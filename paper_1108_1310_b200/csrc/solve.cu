@@ -380,7 +380,8 @@ struct Driver {
     if (K > 1) {
       if (!L.color) throw LamgError(LAMG_E_ERROR, "batched smoothing needs the coloured operator");
       const ExactItems& xi = L.xitems[exact_table_for(K)];
-      if ((int)l < exact_levels() && xi.nitems) bgs_exact(c, L.op.view(), L.sched, xi, b, x, sweeps, K, ws.lv[l].xctl.p);
+      if ((int)l < exact_levels() && L.fcolor) bgs_colored(c, *L.fcolor, L.op.n, b, x, sweeps, K);
+      else if ((int)l < exact_levels() && xi.nitems) bgs_exact(c, L.op.view(), L.sched, xi, b, x, sweeps, K, ws.lv[l].xctl.p);
       else bgs_colored(c, *L.color, L.op.n, b, x, sweeps, K);
     } else if (!exact && L.color && (int)l >= exact_levels()) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
     else gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
