@@ -357,11 +357,10 @@ def run_lamg(args, dist: Dist):
             raise ln.err
         for k, v in kp.items():
             if not tag and k == "gs_finest":
-                # one-column THROUGHPUT solves sweep the finest level in the
-                # reference's exact order (wavefronts, latency-bound) so they
-                # converge in the reference's cycle count; blocks sweep coloured
-                v["note"] = "exact-order wavefront sweep (lamg_ctx_set_exact_levels default 1)"
-                k = "gs_finest_exact_order"
+                # one-column THROUGHPUT solves sweep the finest smoothing level with the same
+                # front-modulo colouring as the blocks (the reference's row order except at the wrap)
+                v["note"] = "front-modulo colouring, one column (64 launches of gs_color kernels per sweep)"
+                k = "gs_finest_one_column"
             kern[k + tag] = v
         log(f"[rank {dist.rank}] profiled {'block' if tag else 'single'} solve in {time.time() - tb:.1f}s")
     if KB > 1 and "gs_finest_block" in kern:
@@ -413,7 +412,7 @@ def run_lamg(args, dist: Dist):
     rhs_per_s = dist.allreduce(float(rhs_done), "SUM") / (max_ms / 1e3)
     sweeps_per_s = dist.allreduce(sweeps_units, "SUM") / (max_ms / 1e3)
 
-    dom = "gs_finest_block" if "gs_finest_block" in kern else ("gs_finest_exact_order" if "gs_finest_exact_order" in kern else None)
+    dom = "gs_finest_block" if "gs_finest_block" in kern else ("gs_finest_one_column" if "gs_finest_one_column" in kern else None)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and args.config == 2 and os.path.exists(tp):  # the captures are of config 2's finest level

@@ -383,7 +383,8 @@ struct Driver {
       if ((int)l < exact_levels() && L.fcolor) bgs_colored(c, *L.fcolor, L.op.n, b, x, sweeps, K);
       else if ((int)l < exact_levels() && xi.nitems) bgs_exact(c, L.op.view(), L.sched, xi, b, x, sweeps, K, ws.lv[l].xctl.p);
       else bgs_colored(c, *L.color, L.op.n, b, x, sweeps, K);
-    } else if (!exact && L.color && (int)l >= exact_levels()) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
+    } else if (!exact && L.fcolor && (int)l < exact_levels()) gs_colored(c, *L.fcolor, L.op.n, b, x, sweeps);
+    else if (!exact && L.color && (int)l >= exact_levels()) gs_colored(c, *L.color, L.op.n, b, x, sweeps);
     else gs_exact(c, L.op.view(), L.sched, b, x, 1, sweeps);
     // algorithmic bytes: operator once (8(n+1) + 24m + 8n) + per column x
     // read, b read, x write (24n); K = 1 gives SURVEY.md 8(d)'s 24m + 40n + 8

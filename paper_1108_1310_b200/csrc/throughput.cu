@@ -996,6 +996,8 @@ void build_direct_inverse(Ctx& c, DDirect& d) {
   c.sync();
 }
 
+static void append_color_ptrs(Ctx& c, int32_t n, DColor& col);
+
 void prepare_throughput(Ctx& c, DHier& h) {
   bool seen_smoother = false;  // the front-modulo colouring serves the finest smoothing level only
   for (size_t l = 0; l < h.levels.size(); ++l) {
@@ -1009,7 +1011,10 @@ void prepare_throughput(Ctx& c, DHier& h) {
     }();
     if (smooths && L.coarsest == CM_NONE && front_mod > 1 && !L.fcolor && !seen_smoother) {
       auto fc = std::make_unique<DColor>();
-      if (build_front_mod_coloring(c, L.op.view(), L.sched, front_mod, *fc)) L.fcolor = std::move(fc);
+      if (build_front_mod_coloring(c, L.op.view(), L.sched, front_mod, *fc)) {
+        append_color_ptrs(c, L.op.n, *fc);
+        L.fcolor = std::move(fc);
+      }
     }
     if (smooths) seen_smoother = true;
     if (smooths && L.coarsest == CM_NONE && !L.xitems[0].rows)
@@ -1020,16 +1025,20 @@ void prepare_throughput(Ctx& c, DHier& h) {
   c.sync();
 }
 
+// append the colour pointers after rp for the single-CTA kernels
+static void append_color_ptrs(Ctx& c, int32_t n, DColor& col) {
+  DVec<int64_t> rp2(n + 1 + (col.ncolors + 2) / 2 + 1, c.s);
+  CK(cudaMemcpyAsync(rp2.p, col.rp.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, c.s));
+  CK(cudaMemcpyAsync(rp2.p + n + 1, col.cptr_h.data(), sizeof(int32_t) * (col.ncolors + 1), cudaMemcpyHostToDevice,
+                     c.s));
+  col.rp = std::move(rp2);
+  c.sync();
+}
+
 std::unique_ptr<DColor> make_color(Ctx& c, const CSRv& a, const Schedule& sch) {
   auto col = std::make_unique<DColor>();
   build_coloring(c, a, sch, *col);
-  // append the colour pointers after rp for the single-CTA kernel
-  DVec<int64_t> rp2(a.n + 1 + (col->ncolors + 2) / 2 + 1, c.s);
-  CK(cudaMemcpyAsync(rp2.p, col->rp.p, sizeof(int64_t) * (a.n + 1), cudaMemcpyDeviceToDevice, c.s));
-  CK(cudaMemcpyAsync(rp2.p + a.n + 1, col->cptr_h.data(), sizeof(int32_t) * (col->ncolors + 1),
-                     cudaMemcpyHostToDevice, c.s));
-  col->rp = std::move(rp2);
-  c.sync();
+  append_color_ptrs(c, a.n, *col);
   return col;
 }
 
