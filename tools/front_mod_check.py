@@ -2,7 +2,7 @@
 colouring (default) against the exact-order block sweep (LAMG_FRONT_MOD=0),
 each in its own process (the setting is read once).
 
-    python tools/front_mod_check.py [cfg|gN] [nrhs]
+    python tools/front_mod_check.py [cfg|gN] [nrhs] [C]
 """
 import json
 import os
@@ -39,11 +39,12 @@ def run(mod, cfg, nrhs):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
     nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 32
-    ex, fm = run(0, cfg, nrhs), run(64, cfg, nrhs)
+    C = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+    ex, fm = run(0, cfg, nrhs), run(C, cfg, nrhs)
     d = [a - b for a, b in zip(fm["cycles"], ex["cycles"])]
     print(f"config {cfg}, {nrhs} right-hand sides")
     print("exact-order block sweep :", ex["cycles"])
-    print("front-modulo, C = 64    :", fm["cycles"])
+    print(f"front-modulo, C = {C:<6}:", fm["cycles"])
     print("difference per column   :", d, " max |diff| =", max(abs(v) for v in d))
     rel = max(abs(a - b) / b for a, b in zip(fm["norm"], ex["norm"]))
     print(f"max relative difference of ||x|| per column: {rel:.3e}")
