@@ -41,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_PEAK_FALLBACK = 6650.0
+FRONT_MOD = int(os.environ.get("LAMG_FRONT_MOD", "32"))  # the library's default (csrc/throughput.cu)
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -359,16 +360,16 @@ def run_lamg(args, dist: Dist):
             if not tag and k == "gs_finest":
                 # one-column THROUGHPUT solves sweep the finest smoothing level with the same
                 # front-modulo colouring as the blocks (the reference's row order except at the wrap)
-                v["note"] = "front-modulo colouring, one column (64 launches of gs_color kernels per sweep)"
+                v["note"] = f"front-modulo colouring, one column ({FRONT_MOD} launches of gs_color kernels per sweep)"
                 k = "gs_finest_one_column"
             kern[k + tag] = v
         log(f"[rank {dist.rank}] profiled {'block' if tag else 'single'} solve in {time.time() - tb:.1f}s")
     if KB > 1 and "gs_finest_block" in kern:
         # the same block with every level swept coloured (lamg_ctx_set_exact_levels(ctx, 0): the
         # HBM-bound form of the finest sweep, which the partitioned solve uses; more cycles)
-        kern["gs_finest_block"]["note"] = ("the benchmarked finest sweep: front-modulo colouring (colour = wavefront mod "
-                                           "64: the reference's row order except at the wrap, 64 launches of "
-                                           "bgs_kernel per sweep; LAMG_FRONT_MOD=0 gives the exact-order bgs_exact)")
+        kern["gs_finest_block"]["note"] = (f"the benchmarked finest sweep: front-modulo colouring (colour = wavefront mod "
+                                           f"{FRONT_MOD}: the reference's row order except at the wrap, {FRONT_MOD} launches "
+                                           "of bgs_kernel per sweep; LAMG_FRONT_MOD=0 gives the exact-order bgs_exact)")
         lanes[0].ctx.set_exact_levels(0)
         kp = kernel_profile(lib, lanes[0], Lane.solve_dev, 0.0)
         torch.cuda.synchronize()

@@ -129,10 +129,11 @@ int lamg_ctx_set_mode(lamg_ctx *ctx, int mode);
  * reference's Gauss-Seidel row order (default 1; 0 = every level greedy-
  * coloured). The first smoothing level's order decides the cycle count
  * (config 2: 129 = the reference's, greedy-coloured 141; RGG 2^20: 13 vs 15).
- * One-column solves sweep those levels in exact order (wavefronts); blocks of
- * columns sweep them with colours = wavefront mod 64 (the reference's order
- * except at the wrap; environment LAMG_FRONT_MOD, 0 = exact order by
- * ticketed wavefront items). Partitioned solves sweep greedy-coloured. */
+ * Those levels are swept with colours = wavefront mod 32 (the reference's
+ * order except at the wrap; environment LAMG_FRONT_MOD, 0 = exact order:
+ * wavefront kernel for one column, ticketed wavefront items for blocks), and
+ * in exact order where that is not a proper colouring. Partitioned solves
+ * sweep greedy-coloured. */
 int lamg_ctx_set_exact_levels(lamg_ctx *ctx, int32_t levels);
 void lamg_ctx_destroy(lamg_ctx *ctx);
 const char *lamg_last_error(void);

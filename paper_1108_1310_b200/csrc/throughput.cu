@@ -147,7 +147,7 @@ void build_coloring(Ctx& c, const CSRv& a, const Schedule& sch, DColor& out) {
   build_coloring_from(c, a, color, out);
 }
 
-// Front-modulo colouring (LAMG_FRONT_MOD=C, default 64) of the finest smoothing level for
+// Front-modulo colouring (LAMG_FRONT_MOD=C, default 32) of the finest smoothing level for
 // K-column blocks: colour(u) = front(u) mod C, where front(u) is u's wavefront in the
 // exact-order schedule. A row of colour c sees its lower neighbours (front f - 1: colour
 // c - 1) already swept and its upper neighbours (front f + 1: colour c + 1) not yet, exactly
@@ -1007,7 +1007,7 @@ void prepare_throughput(Ctx& c, DHier& h) {
     if (smooths && !L.color) L.color = make_color(c, L.op.view(), L.sched);
     static const int front_mod = [] {
       const char* e = getenv("LAMG_FRONT_MOD");
-      return e ? atoi(e) : 64;  // 0 / 1: K-column blocks sweep the level with bgs_exact instead
+      return e ? atoi(e) : 32;  // 0 / 1: the level is swept in exact order (bgs_exact, wavefront kernels) instead
     }();
     if (smooths && L.coarsest == CM_NONE && front_mod > 1 && !L.fcolor && !seen_smoother) {
       auto fc = std::make_unique<DColor>();
